@@ -1,0 +1,197 @@
+/*
+ * mcb.h — C-ABI drop-in boundary for the direct Monte Carlo multi-function
+ * integration path (arXiv 2104.10073, ZMCintegral-v5.1 "multifunctions"),
+ * B200-native (sm_100a).
+ *
+ * The reference (`/root/reference/proj`, library `mcbatch`) exposes this path
+ * only as a C++ header API; there is no FFI.  Each entry point below names the
+ * reference interface it replaces (file:line, relative to
+ * /root/reference/proj).  Plain pointers and sizes, caller-allocated buffers,
+ * status codes instead of exceptions; no torch or CUDA types in signatures
+ * (streams are passed as `void*` = cudaStream_t).
+ *
+ * Integrands are *family descriptors* instead of free DSL strings; every
+ * descriptor lowers (mcb_to_dsl) to the exact DSL source the reference would
+ * parse, and the device evaluator follows the same left-to-right operation
+ * order as the reference's compiled postfix program (src/expr.cpp:520-553).
+ */
+#ifndef MCB_MCB_H_
+#define MCB_MCB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCB_ABI_VERSION 1u
+
+#if defined(__GNUC__)
+#define MCB_API __attribute__((visibility("default")))
+#else
+#define MCB_API
+#endif
+
+/* Samples per (key, chunk): include/mcbatch/sampling.hpp:11 (kChunkSize). */
+#define MCB_CHUNK_SIZE 65536u
+/* Largest supported dimension of a family descriptor. */
+#define MCB_MAX_DIM 8u
+/* Non-finite warning fraction: include/mcbatch/estimator.hpp:16. */
+#define MCB_NONFINITE_WARN_FRACTION 0.01
+
+typedef enum mcb_status {
+  MCB_OK = 0,
+  MCB_ERR_INVALID_ARGUMENT = 1, /* bad pointer/size/descriptor; see mcb_last_error */
+  MCB_ERR_VALIDATION = 2,       /* job failed validation (reference ValidationError) */
+  MCB_ERR_CUDA = 3,             /* CUDA runtime / launch failure */
+  MCB_ERR_NO_DEVICE = 4,        /* no usable sm_100 device */
+  MCB_ERR_OUT_OF_RANGE = 5,     /* chunk index > 2^32-1 (src/sampling.cpp:80-81) */
+  MCB_ERR_BUFFER_TOO_SMALL = 6
+} mcb_status;
+
+/* Built-in integrand families (BASELINE.json north_star; Eq.1/Eq.2).
+ * DSL lowering (mcb_to_dsl), with x1..xd the coordinates:
+ *   HARMONIC      "a*cos(k*(x1+...+xd)) + b*sin(k*(x1+...+xd))"
+ *                 or, when flags has MCB_FLAG_UNIT_COEFFS (a = b = 1),
+ *                 "cos(k*(x1+...+xd)) + sin(k*(x1+...+xd))"   (src/job_io.cpp:367)
+ *   HARMONIC_VEC  "a*cos(k1*x1+...+kd*xd) + b*sin(k1*x1+...+kd*xd)"
+ *   ABS2          "a*abs(x1+x2)"   ("abs(x1+x2)" when a == 1), dim >= 2
+ *   ABS3          "a*abs(x1+x2-x3)" ("abs(x1+x2-x3)" when a == 1), dim >= 3
+ */
+typedef enum mcb_family {
+  MCB_FAMILY_HARMONIC = 0,
+  MCB_FAMILY_HARMONIC_VEC = 1,
+  MCB_FAMILY_ABS2 = 2,
+  MCB_FAMILY_ABS3 = 3
+} mcb_family;
+
+#define MCB_FLAG_UNIT_COEFFS 0x1u
+
+/* One integrand = one reference IntegrandSpec (include/mcbatch/batch.hpp:22-31)
+ * restricted to Method::Direct and a family descriptor.  `integrand_index` is
+ * the StreamKey integrand index (= the job-list position in the reference,
+ * src/batch.cpp:221); it is explicit so that shards of a job keep the global
+ * stream identity. */
+typedef struct mcb_integrand {
+  uint32_t family;          /* mcb_family */
+  uint32_t dim;             /* 1..MCB_MAX_DIM */
+  uint32_t integrand_index; /* StreamKey.integrand_index */
+  uint32_t flags;           /* MCB_FLAG_* */
+  uint64_t n_samples;       /* per trial, >= 2 */
+  double a, b;              /* coefficients (ABS families use `a`) */
+  double k[MCB_MAX_DIM];    /* HARMONIC: k[0]; HARMONIC_VEC: k[0..dim-1] */
+  double low[MCB_MAX_DIM];  /* HyperRect low  (include/mcbatch/sampling.hpp:14-24) */
+  double high[MCB_MAX_DIM]; /* HyperRect high */
+} mcb_integrand;
+
+enum { MCB_TRIAL_OK = 0, MCB_TRIAL_ALL_NONFINITE = 1 };
+
+/* Per-(integrand, trial) result = reference McEstimate
+ * (include/mcbatch/estimator.hpp:18-25) plus a status replacing the
+ * AllSamplesNonFinite exception (src/estimator.cpp:58-59). */
+typedef struct mcb_trial_stats {
+  double value;       /* volume * mean */
+  double std_error;   /* volume * sqrt((m2/(n-1))/n); +inf when n < 2 */
+  uint64_t n_samples; /* finite + non-finite */
+  uint64_t n_nonfinite;
+  uint32_t status;    /* MCB_TRIAL_* */
+  uint32_t nonfinite_warning;
+} mcb_trial_stats;
+
+/* One validation problem (reference Violation, include/mcbatch/batch.hpp:40-44).
+ * integrand = -1 for job-level problems. */
+typedef struct mcb_violation {
+  int64_t integrand;
+  char message[120];
+} mcb_violation;
+
+/* ---- introspection ------------------------------------------------------ */
+MCB_API uint32_t mcb_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+MCB_API const char* mcb_last_error(void);
+/* Number of visible CUDA devices (0 when none or the driver is absent). */
+MCB_API int mcb_device_count(void);
+
+/* ---- host-side helpers (no GPU needed) ---------------------------------- */
+/* Cipher key of (seed, integrand): src/sampling.cpp:84-87. */
+MCB_API void mcb_stream_key(uint64_t global_seed, uint32_t integrand_index, uint32_t key_out[2]);
+/* HyperRect::volume, left-to-right product from 1.0: src/sampling.cpp:16-20. */
+MCB_API double mcb_volume(const mcb_integrand* fn);
+/* Exact reference DSL source for a descriptor; returns bytes needed incl. NUL. */
+MCB_API size_t mcb_to_dsl(const mcb_integrand* fn, char* buf, size_t cap);
+/* Reference validate() (src/batch.cpp:62-120) for a direct family job.
+ * Writes up to `cap` violations, sets *n_out to the total found.
+ * `names` may be NULL (then integrands are named by position, and the
+ * duplicate-name check is skipped). Returns MCB_OK even if violations exist. */
+MCB_API mcb_status mcb_validate(const mcb_integrand* fns, size_t n_fns, const char* const* names,
+                        uint32_t trials, mcb_violation* out, size_t cap, size_t* n_out);
+/* LPT shard assignment of integrands to `n_shards` devices by estimated cost
+ * n_samples * trials * per-sample cost(family, dim).  Deterministic. */
+MCB_API mcb_status mcb_partition(const mcb_integrand* fns, size_t n_fns, uint32_t trials,
+                         int n_shards, uint32_t* shard_of_fn);
+/* summarize_trials (src/estimator.cpp:320-337) over the OK trials in order. */
+MCB_API mcb_status mcb_summarize_trials(const mcb_trial_stats* per_trial, uint32_t n_trials,
+                                double* mean, double* trial_stddev, uint32_t* n_ok);
+
+/* ---- the hot path -------------------------------------------------------- */
+/* run_batch Direct branch (src/batch.cpp:195-333): every integrand, every
+ * trial t in [0, trials), StreamKey {seed, integrand_index, t, chunk}.
+ * `out` is n_fns*trials, row-major by integrand.  Devices: `devices` lists
+ * CUDA ordinals (NULL/0 = device 0); one host thread per entry, integrands
+ * sharded by mcb_partition; results are byte-identical for any device list.
+ * Synchronous.  `seconds` (may be NULL) receives the wall time of the
+ * sampling phase (reference BatchResult.total_seconds). */
+MCB_API mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
+                          uint32_t trials, const int* devices, int n_devices,
+                          mcb_trial_stats* out, double* seconds);
+
+/* direct_mc (src/estimator.cpp:75-92) for one integrand and one key base
+ * {seed, fn->integrand_index, trial, chunk_base}, on `device`. */
+MCB_API mcb_status mcb_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
+                         uint64_t chunk_base, int device, mcb_trial_stats* out);
+
+/* ---- device-resident plans (descriptors stay in HBM; async on a stream) -- */
+typedef struct mcb_plan mcb_plan;
+typedef struct mcb_plan_info {
+  uint64_t n_fns;
+  uint32_t trials;
+  uint32_t n_groups;        /* (family, dim) kernel launches per run */
+  uint64_t n_tiles;         /* (fn, trial, chunk) work units */
+  uint64_t total_samples;   /* sum n_samples * trials */
+  uint64_t philox_blocks;   /* sum over tiles of ceil(count*dim/2) */
+  uint32_t launches_per_run;/* kernels launched by mcb_plan_launch */
+  uint32_t reserved;
+} mcb_plan_info;
+
+MCB_API mcb_status mcb_plan_create(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
+                           uint32_t trials, int device, mcb_plan** plan_out);
+/* Enqueue the fused sample->eval->reduce kernels plus the ordered chunk
+ * combine on `stream` (NULL = legacy default stream).  No host sync. */
+MCB_API mcb_status mcb_plan_launch(mcb_plan* plan, void* stream);
+/* Copy the n_fns*trials results to host (synchronizes `stream`). */
+MCB_API mcb_status mcb_plan_download(mcb_plan* plan, mcb_trial_stats* out, void* stream);
+MCB_API mcb_status mcb_plan_get_info(const mcb_plan* plan, mcb_plan_info* info);
+MCB_API void mcb_plan_destroy(mcb_plan* plan);
+
+/* ---- test / measurement hooks ------------------------------------------- */
+/* sample_uniform (src/sampling.cpp:102-112) on the GPU: `count` points of
+ * `dim` coordinates starting at point `first_point` of chunk `chunk`,
+ * row-major into host `out` (count*dim doubles).  Used for bit-exact tests. */
+MCB_API mcb_status mcb_debug_points(uint64_t seed, uint32_t integrand_index, uint32_t trial,
+                            uint64_t chunk, uint64_t first_point, uint64_t count,
+                            uint32_t dim, const double* low, const double* high,
+                            int device, double* out);
+/* Per-sample family values f(x) for the same points (device evaluator). */
+MCB_API mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
+                          uint64_t chunk, uint64_t first_point, uint64_t count,
+                          int device, double* out);
+/* Microbenchmark of the integer multiply pipe that bounds Philox:
+ * 32x32->64 multiplies per second on `device` over ~`ms` milliseconds. */
+MCB_API mcb_status mcb_probe_mul_peak(int device, double ms, double* muls_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MCB_MCB_H_ */

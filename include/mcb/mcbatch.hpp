@@ -1,0 +1,188 @@
+// mcbatch.hpp — C++ host API mirroring the reference `mcbatch` direct path
+// (/root/reference/proj/include/mcbatch/{sampling,estimator,batch,job_io}.hpp),
+// implemented over the C-ABI in mcb.h and executed by the sm_100a kernels.
+//
+// Differences from the reference, all deliberate:
+//  * IntegrandSpec carries a family descriptor (`family` + `params` map using
+//    the DSL parameter names a, b, k, k1..kd) instead of free DSL source;
+//    `source()` returns the exact DSL the reference would parse, and
+//    `IntegrandSpec::from_source()` recognises those sources.
+//  * JobSpec::workers (CPU threads) becomes JobSpec::devices (CUDA ordinals).
+//    Results are byte-identical for any device list, the analogue of the
+//    reference's worker invariance (tests/test_batch.cpp:91-121).
+//  * Only Method::Direct exists (stratified/tree are out of scope).
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mcb/mcb.h"
+
+namespace mcb {
+
+inline constexpr std::size_t kChunkSize = MCB_CHUNK_SIZE;             // sampling.hpp:11
+inline constexpr double kNonFiniteWarnFraction = MCB_NONFINITE_WARN_FRACTION;  // estimator.hpp:16
+
+// include/mcbatch/sampling.hpp:14-24
+struct HyperRect {
+  std::vector<double> low;
+  std::vector<double> high;
+
+  std::size_t dim() const { return low.size(); }
+  bool valid() const;
+  double volume() const;
+
+  static HyperRect unit(std::size_t d);
+  static HyperRect box(std::vector<double> lo, std::vector<double> hi);
+};
+
+struct InvalidDomain : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// include/mcbatch/sampling.hpp:33-44
+struct StreamKey {
+  std::uint64_t global_seed = 0;
+  std::uint32_t integrand_index = 0;
+  std::uint32_t trial_index = 0;
+  std::uint64_t chunk_index = 0;
+
+  StreamKey with_chunk(std::uint64_t c) const {
+    StreamKey k = *this;
+    k.chunk_index = c;
+    return k;
+  }
+};
+
+// sample_uniform (src/sampling.cpp:102-112), computed on the GPU.
+std::vector<double> sample_uniform(const HyperRect& rect, const StreamKey& key, std::size_t count,
+                                   int device = 0);
+
+enum class Family {
+  Harmonic = MCB_FAMILY_HARMONIC,         // a*cos(k*(x1+..+xd)) + b*sin(k*(x1+..+xd))
+  HarmonicVec = MCB_FAMILY_HARMONIC_VEC,  // a*cos(k1*x1+..+kd*xd) + b*sin(...)
+  Abs2 = MCB_FAMILY_ABS2,                 // a*abs(x1+x2)
+  Abs3 = MCB_FAMILY_ABS3                  // a*abs(x1+x2-x3)
+};
+
+enum class Method { Direct };
+const char* method_name(Method m);
+
+// include/mcbatch/batch.hpp:22-31 with a family descriptor.
+struct IntegrandSpec {
+  std::string name;
+  Family family = Family::Harmonic;
+  bool unit_coeffs = false;  // Harmonic only: the Fig.1 form cos(..) + sin(..)
+  std::size_t dim = 1;
+  HyperRect domain;
+  std::map<std::string, double> params;  // a, b, k | a, b, k1..kd | a
+  std::uint64_t n_samples = 10000;
+  Method method = Method::Direct;
+
+  // Exact reference DSL source of this descriptor.
+  std::string source() const;
+  // Recognise a reference DSL source of one of the families (whitespace
+  // insensitive); throws std::invalid_argument for anything else.
+  static IntegrandSpec from_source(std::string name, const std::string& source, std::size_t dim,
+                                   HyperRect domain, std::map<std::string, double> params,
+                                   std::uint64_t n_samples);
+};
+
+struct JobSpec {
+  std::uint64_t seed = 0;
+  std::uint32_t trials = 1;
+  std::vector<int> devices;  // empty = {0}
+  std::vector<IntegrandSpec> integrands;
+};
+
+struct Violation {
+  std::string integrand;  // empty for job-level problems
+  std::string message;
+};
+
+std::vector<Violation> validate(const JobSpec& job);
+
+struct ValidationError : std::runtime_error {
+  std::vector<Violation> violations;
+  explicit ValidationError(std::vector<Violation> v);
+};
+
+// include/mcbatch/estimator.hpp:18-31
+struct McEstimate {
+  double value = 0.0;
+  double std_error = 0.0;
+  std::uint64_t n_samples = 0;
+  std::uint64_t n_nonfinite = 0;
+  bool nonfinite_warning = false;
+  bool budget_exhausted = false;
+};
+
+struct TrialSummary {
+  std::vector<McEstimate> per_trial;
+  double mean = 0.0;
+  double trial_stddev = 0.0;
+};
+
+struct AllSamplesNonFinite : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InsufficientTrials : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// A CUDA / device failure (there is no CPU fallback).
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// include/mcbatch/batch.hpp:53-66
+struct IntegrandResult {
+  std::string name;
+  bool ok = false;
+  std::string error;
+  TrialSummary summary;
+  double seconds = 0.0;  // cost-weighted share of the batch's sampling time
+  bool nonfinite_warning = false;
+  bool budget_exhausted = false;
+};
+
+struct BatchResult {
+  std::vector<IntegrandResult> per_integrand;  // job order
+  double total_seconds = 0.0;
+};
+
+// src/batch.cpp:195-333
+BatchResult run_batch(const JobSpec& job);
+
+// src/batch.cpp:335-367
+std::vector<TrialSummary> parameter_scan(const IntegrandSpec& tmpl, const std::string& param_name,
+                                         std::span<const double> values, std::uint32_t trials,
+                                         std::uint64_t seed, std::vector<int> devices = {});
+
+// src/estimator.cpp:75-92; throws AllSamplesNonFinite like the reference.
+McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const StreamKey& key_base,
+                     int device = 0);
+
+// src/estimator.cpp:320-337
+TrialSummary summarize_trials(std::vector<McEstimate> per_trial);
+
+// src/estimator.cpp:339-355
+TrialSummary repeated_trials(const std::function<McEstimate(std::uint32_t)>& run,
+                             std::uint32_t trials);
+
+std::uint64_t chunk_count(std::uint64_t n_samples);
+
+// src/job_io.cpp:336-376 (harmonic benchmark family of Fig. 1)
+double harmonic_k(std::uint32_t n);
+double harmonic_closed_form(double k, std::size_t dim = 4);
+double analytic_harmonic(std::uint32_t n);
+JobSpec make_harmonic_job(std::uint32_t n_count, std::uint64_t samples);
+
+// Lowering to the C-ABI descriptor (integrand_index = list position).
+mcb_integrand to_descriptor(const IntegrandSpec& spec, std::uint32_t integrand_index);
+
+}  // namespace mcb

@@ -1,0 +1,205 @@
+// ref_shim.cpp — extern "C" shim over the UNMODIFIED reference library.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file
+// together with the reference's own sources, read in place from
+// /root/reference/proj/src/{expr,sampling,estimator,batch,job_io}.cpp, into
+// oracle/_ref/libmcbatch_ref.so (git-ignored; never shipped in the product).
+// It exists so that (1) tests/golden/make_golden.py can dump golden vectors
+// produced by the reference itself and (2) bench.py's cpu_baseline and
+// `--impl reference` legs time the reference's own run_batch
+// (src/batch.cpp:195-333) with its own thread pool.
+//
+// No reference source is copied here: this file only includes the public
+// headers (include/mcbatch/*.hpp) and calls the public API.
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "mcb/mcb.h"
+#include "mcbatch/batch.hpp"
+#include "mcbatch/estimator.hpp"
+#include "mcbatch/expr.hpp"
+#include "mcbatch/job_io.hpp"
+#include "mcbatch/sampling.hpp"
+
+using namespace mcbatch;
+
+namespace {
+
+thread_local std::string g_err;
+
+HyperRect rect_of(std::uint32_t dim, const double* lo, const double* hi) {
+  HyperRect r;
+  r.low.assign(lo, lo + dim);
+  r.high.assign(hi, hi + dim);
+  return r;
+}
+
+// Parameter binding for a family descriptor (names as in mcb_to_dsl).
+std::map<std::string, double> params_of(const mcb_integrand& f) {
+  std::map<std::string, double> p;
+  switch (f.family) {
+    case MCB_FAMILY_HARMONIC:
+      p["k"] = f.k[0];
+      if (!(f.flags & MCB_FLAG_UNIT_COEFFS)) {
+        p["a"] = f.a;
+        p["b"] = f.b;
+      }
+      break;
+    case MCB_FAMILY_HARMONIC_VEC:
+      p["a"] = f.a;
+      p["b"] = f.b;
+      for (std::uint32_t j = 0; j < f.dim; ++j) p["k" + std::to_string(j + 1)] = f.k[j];
+      break;
+    default:
+      p["a"] = f.a;
+      break;
+  }
+  return p;
+}
+
+void fill(const McEstimate& e, mcb_trial_stats* st) {
+  st->value = e.value;
+  st->std_error = e.std_error;
+  st->n_samples = e.n_samples;
+  st->n_nonfinite = e.n_nonfinite;
+  st->status = MCB_TRIAL_OK;
+  st->nonfinite_warning = e.nonfinite_warning ? 1u : 0u;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// sample_uniform (src/sampling.cpp:102-112) with StreamKey {seed, i, t, c}.
+int ref_sample_uniform(std::uint32_t dim, const double* lo, const double* hi,
+                       std::uint64_t seed, std::uint32_t integrand, std::uint32_t trial,
+                       std::uint64_t chunk, std::uint64_t count, double* out) {
+  try {
+    std::vector<double> pts =
+        sample_uniform(rect_of(dim, lo, hi), StreamKey{seed, integrand, trial, chunk}, count);
+    std::memcpy(out, pts.data(), pts.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// CompiledProgram::evaluate (src/expr.cpp:520-553) of `source` on n points.
+int ref_eval_points(const char* source, const mcb_integrand* f, const double* pts,
+                    std::uint64_t n, double* out) {
+  try {
+    auto pm = params_of(*f);
+    std::vector<std::string> names;
+    std::vector<double> vals;
+    for (auto& [k, v] : pm) { names.push_back(k); vals.push_back(v); }
+    CompiledProgram prog = compile(parse(source), f->dim, names);
+    std::vector<double> stack;
+    for (std::uint64_t i = 0; i < n; ++i)
+      out[i] = prog.evaluate({pts + i * f->dim, f->dim}, vals, stack);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// direct_mc (src/estimator.cpp:75-92) of the lowered family source.
+int ref_direct_mc(const char* source, const mcb_integrand* f, std::uint64_t seed,
+                  std::uint32_t trial, std::uint64_t chunk_base, mcb_trial_stats* out) {
+  try {
+    auto pm = params_of(*f);
+    std::vector<std::string> names;
+    std::vector<double> vals;
+    for (auto& [k, v] : pm) { names.push_back(k); vals.push_back(v); }
+    CompiledProgram prog = compile(parse(source), f->dim, names);
+    std::memset(out, 0, sizeof *out);
+    try {
+      McEstimate e = direct_mc(prog, vals, rect_of(f->dim, f->low, f->high), f->n_samples,
+                               StreamKey{seed, f->integrand_index, trial, chunk_base});
+      fill(e, out);
+    } catch (const AllSamplesNonFinite&) {
+      out->status = MCB_TRIAL_ALL_NONFINITE;
+      out->n_samples = f->n_samples;
+      out->n_nonfinite = f->n_samples;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// run_batch (src/batch.cpp:195-333) of n integrands given as lowered sources
+// + descriptors (integrand_index must equal the list position, as in the
+// reference).  out_trials: n*trials McEstimates (status ALL_NONFINITE for a
+// failed trial); out_mean/out_sd/out_ok per integrand; *seconds =
+// BatchResult.total_seconds.
+int ref_run_batch(const char* const* sources, const mcb_integrand* fns, std::size_t n,
+                  std::uint64_t seed, std::uint32_t trials, std::uint32_t workers,
+                  mcb_trial_stats* out_trials, double* out_mean, double* out_sd,
+                  std::int32_t* out_ok, double* seconds) {
+  try {
+    JobSpec job;
+    job.seed = seed;
+    job.trials = trials;
+    job.workers = workers;
+    for (std::size_t i = 0; i < n; ++i) {
+      IntegrandSpec s;
+      s.name = "f" + std::to_string(i);
+      s.source = sources[i];
+      s.dim = fns[i].dim;
+      s.domain = rect_of(fns[i].dim, fns[i].low, fns[i].high);
+      s.params = params_of(fns[i]);
+      s.n_samples = fns[i].n_samples;
+      s.method = Method::Direct;
+      job.integrands.push_back(std::move(s));
+    }
+    BatchResult br = run_batch(job);
+    for (std::size_t i = 0; i < n; ++i) {
+      const IntegrandResult& r = br.per_integrand[i];
+      out_ok[i] = r.ok ? 1 : 0;
+      out_mean[i] = r.ok ? r.summary.mean : NAN;
+      out_sd[i] = r.ok ? r.summary.trial_stddev : NAN;
+      for (std::uint32_t t = 0; t < trials; ++t) std::memset(&out_trials[i * trials + t], 0, sizeof(mcb_trial_stats));
+      // per_trial holds only the successful trials, in ascending order; a
+      // fully successful integrand has exactly `trials` of them.
+      if (r.ok && r.summary.per_trial.size() == trials)
+        for (std::uint32_t t = 0; t < trials; ++t)
+          fill(r.summary.per_trial[t], &out_trials[i * trials + t]);
+    }
+    if (seconds) *seconds = br.total_seconds;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// make_harmonic_job (src/job_io.cpp:355-376): the reference's own k_n values.
+int ref_harmonic_job(std::uint32_t n_count, std::uint64_t samples, double* k_out,
+                     std::uint64_t* seed_out, std::uint32_t* trials_out) {
+  try {
+    JobSpec job = make_harmonic_job(n_count, samples);
+    for (std::uint32_t i = 0; i < n_count; ++i) k_out[i] = job.integrands[i].params.at("k");
+    *seed_out = job.seed;
+    *trials_out = job.trials;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+double ref_harmonic_closed_form(double k) { return harmonic_closed_form(k); }
+double ref_analytic_harmonic(std::uint32_t n) { return analytic_harmonic(n); }
+
+}  // extern "C"

@@ -1,0 +1,303 @@
+"""B200-native direct Monte Carlo multi-function integration (arXiv 2104.10073).
+
+Python view of the C-ABI in ``include/mcb/mcb.h`` (ctypes over the in-tree
+``libmcb.so``).  The library is the product: sm_100a kernels behind a C ABI,
+with no CPU fallback — importing this package without the built library
+raises, and compute calls without a B200 return ``MCB_ERR_NO_DEVICE``.
+
+Reference correspondence (``/root/reference/proj``):
+``run_direct`` ~ ``run_batch`` Direct branch (src/batch.cpp:195-333),
+``direct_mc`` ~ src/estimator.cpp:75-92, ``debug_points`` ~ ``sample_uniform``
+(src/sampling.cpp:102-112), ``make_harmonic_job`` ~ src/job_io.cpp:355-376.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmcb.so")
+
+CHUNK_SIZE = 65536
+MAX_DIM = 8
+
+FAMILY_HARMONIC = 0
+FAMILY_HARMONIC_VEC = 1
+FAMILY_ABS2 = 2
+FAMILY_ABS3 = 3
+FLAG_UNIT_COEFFS = 1
+
+TRIAL_OK = 0
+TRIAL_ALL_NONFINITE = 1
+
+STATUS = {0: "MCB_OK", 1: "MCB_ERR_INVALID_ARGUMENT", 2: "MCB_ERR_VALIDATION", 3: "MCB_ERR_CUDA",
+          4: "MCB_ERR_NO_DEVICE", 5: "MCB_ERR_OUT_OF_RANGE", 6: "MCB_ERR_BUFFER_TOO_SMALL"}
+
+
+class McbError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+class Integrand(ctypes.Structure):
+    """``mcb_integrand`` (include/mcb/mcb.h)."""
+    _fields_ = [("family", ctypes.c_uint32), ("dim", ctypes.c_uint32),
+                ("integrand_index", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+                ("n_samples", ctypes.c_uint64), ("a", ctypes.c_double), ("b", ctypes.c_double),
+                ("k", ctypes.c_double * MAX_DIM), ("low", ctypes.c_double * MAX_DIM),
+                ("high", ctypes.c_double * MAX_DIM)]
+
+
+class TrialStats(ctypes.Structure):
+    """``mcb_trial_stats`` = reference McEstimate + status."""
+    _fields_ = [("value", ctypes.c_double), ("std_error", ctypes.c_double),
+                ("n_samples", ctypes.c_uint64), ("n_nonfinite", ctypes.c_uint64),
+                ("status", ctypes.c_uint32), ("nonfinite_warning", ctypes.c_uint32)]
+
+
+class Violation(ctypes.Structure):
+    _fields_ = [("integrand", ctypes.c_int64), ("message", ctypes.c_char * 120)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n_fns", ctypes.c_uint64), ("trials", ctypes.c_uint32),
+                ("n_groups", ctypes.c_uint32), ("n_tiles", ctypes.c_uint64),
+                ("total_samples", ctypes.c_uint64), ("philox_blocks", ctypes.c_uint64),
+                ("launches_per_run", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+TRIAL_DTYPE = np.dtype([("value", "<f8"), ("std_error", "<f8"), ("n_samples", "<u8"),
+                        ("n_nonfinite", "<u8"), ("status", "<u4"), ("nonfinite_warning", "<u4")])
+assert TRIAL_DTYPE.itemsize == ctypes.sizeof(TrialStats)
+
+# Every symbol include/mcb/mcb.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = [
+    "mcb_abi_version", "mcb_last_error", "mcb_device_count", "mcb_stream_key", "mcb_volume",
+    "mcb_to_dsl", "mcb_validate", "mcb_partition", "mcb_summarize_trials", "mcb_run_direct",
+    "mcb_direct_mc", "mcb_plan_create", "mcb_plan_launch", "mcb_plan_download",
+    "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
+    "mcb_probe_mul_peak",
+]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(or make -C paper_2104_10073_b200/csrc). There is no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    u32, u64, i32, dbl, vp, sz = (ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_double,
+                                  ctypes.c_void_p, ctypes.c_size_t)
+    sig = {
+        "mcb_abi_version": (u32, []),
+        "mcb_last_error": (ctypes.c_char_p, []),
+        "mcb_device_count": (i32, []),
+        "mcb_stream_key": (None, [u64, u32, P(u32)]),
+        "mcb_volume": (dbl, [P(Integrand)]),
+        "mcb_to_dsl": (sz, [P(Integrand), ctypes.c_char_p, sz]),
+        "mcb_validate": (i32, [P(Integrand), sz, P(ctypes.c_char_p), u32, P(Violation), sz, P(sz)]),
+        "mcb_partition": (i32, [P(Integrand), sz, u32, i32, P(u32)]),
+        "mcb_summarize_trials": (i32, [P(TrialStats), u32, P(dbl), P(dbl), P(u32)]),
+        "mcb_run_direct": (i32, [P(Integrand), sz, u64, u32, P(i32), i32, vp, P(dbl)]),
+        "mcb_direct_mc": (i32, [P(Integrand), u64, u32, u64, i32, P(TrialStats)]),
+        "mcb_plan_create": (i32, [P(Integrand), sz, u64, u32, i32, P(vp)]),
+        "mcb_plan_launch": (i32, [vp, vp]),
+        "mcb_plan_download": (i32, [vp, vp, vp]),
+        "mcb_plan_get_info": (i32, [vp, P(PlanInfo)]),
+        "mcb_plan_destroy": (None, [vp]),
+        "mcb_debug_points": (i32, [u64, u32, u32, u64, u64, u64, u32, P(dbl), P(dbl), i32, vp]),
+        "mcb_debug_eval": (i32, [P(Integrand), u64, u32, u64, u64, u64, i32, vp]),
+        "mcb_probe_mul_peak": (i32, [i32, dbl, P(dbl)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise McbError(status, lib.mcb_last_error().decode())
+
+
+def device_count() -> int:
+    return int(lib.mcb_device_count())
+
+
+# ---------------------------------------------------------------- descriptors
+
+def make_integrand(family: int, dim: int, *, k=0.0, a: float = 1.0, b: float = 1.0,
+                   low: Optional[Sequence[float]] = None, high: Optional[Sequence[float]] = None,
+                   n_samples: int = 10000, index: int = 0, unit_coeffs: bool = False) -> Integrand:
+    f = Integrand()
+    f.family, f.dim, f.integrand_index = family, dim, index
+    f.flags = FLAG_UNIT_COEFFS if unit_coeffs else 0
+    f.n_samples = n_samples
+    f.a, f.b = a, b
+    ks = list(k) if isinstance(k, (list, tuple, np.ndarray)) else [k]
+    for j, v in enumerate(ks):
+        f.k[j] = v
+    lo = [0.0] * dim if low is None else list(low)
+    hi = [1.0] * dim if high is None else list(high)
+    for j in range(dim):
+        f.low[j], f.high[j] = lo[j], hi[j]
+    return f
+
+
+def harmonic(k: float, dim: int = 4, *, a: float = 1.0, b: float = 1.0, unit_coeffs=None,
+             low=None, high=None, n_samples: int = 10000, index: int = 0) -> Integrand:
+    """a*cos(k*(x1+..+xd)) + b*sin(k*(x1+..+xd)); unit_coeffs -> the Fig.1 form."""
+    if unit_coeffs is None:
+        unit_coeffs = (a == 1.0 and b == 1.0)
+    return make_integrand(FAMILY_HARMONIC, dim, k=k, a=a, b=b, low=low, high=high,
+                          n_samples=n_samples, index=index, unit_coeffs=unit_coeffs)
+
+
+def to_dsl(f: Integrand) -> str:
+    n = lib.mcb_to_dsl(ctypes.byref(f), None, 0)
+    buf = ctypes.create_string_buffer(n)
+    lib.mcb_to_dsl(ctypes.byref(f), buf, n)
+    return buf.value.decode()
+
+
+def volume(f: Integrand) -> float:
+    return float(lib.mcb_volume(ctypes.byref(f)))
+
+
+def stream_key(seed: int, integrand_index: int):
+    key = (ctypes.c_uint32 * 2)()
+    lib.mcb_stream_key(seed, integrand_index, key)
+    return int(key[0]), int(key[1])
+
+
+def as_array(fns: Sequence[Integrand]):
+    if isinstance(fns, ctypes.Array):
+        return fns
+    arr = (Integrand * len(fns))()
+    for i, f in enumerate(fns):
+        arr[i] = f
+    return arr
+
+
+def validate(fns: Sequence[Integrand], trials: int, names: Optional[Sequence[str]] = None):
+    arr = as_array(fns)
+    cap = 8 * len(arr) + 8
+    out = (Violation * cap)()
+    n = ctypes.c_size_t()
+    cn = None
+    if names is not None:
+        cn = (ctypes.c_char_p * len(names))(*[s.encode() for s in names])
+    _check(lib.mcb_validate(arr, len(arr), cn, trials, out, cap, ctypes.byref(n)))
+    return [(int(out[i].integrand), out[i].message.decode()) for i in range(min(n.value, cap))]
+
+
+def partition(fns: Sequence[Integrand], trials: int, n_shards: int) -> np.ndarray:
+    arr = as_array(fns)
+    out = (ctypes.c_uint32 * len(arr))()
+    _check(lib.mcb_partition(arr, len(arr), trials, n_shards, out))
+    return np.frombuffer(out, dtype=np.uint32).copy()
+
+
+def summarize_trials(per_trial: np.ndarray):
+    arr = np.ascontiguousarray(per_trial, dtype=TRIAL_DTYPE)
+    mean, sd, nok = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint32()
+    _check(lib.mcb_summarize_trials(arr.ctypes.data_as(ctypes.POINTER(TrialStats)), len(arr),
+                                    ctypes.byref(mean), ctypes.byref(sd), ctypes.byref(nok)))
+    return mean.value, sd.value, nok.value
+
+
+# ---------------------------------------------------------------- hot path
+
+def run_direct(fns: Sequence[Integrand], seed: int, trials: int,
+               devices: Optional[Sequence[int]] = None, return_seconds: bool = False):
+    """All integrands x trials on the GPU(s); returns a (n_fns, trials) TRIAL_DTYPE array."""
+    arr = as_array(fns)
+    out = np.zeros((len(arr), trials), dtype=TRIAL_DTYPE)
+    secs = ctypes.c_double()
+    if devices:
+        dv = (ctypes.c_int * len(devices))(*devices)
+        nd = len(devices)
+    else:
+        dv, nd = None, 0
+    _check(lib.mcb_run_direct(arr, len(arr), seed, trials, dv, nd, out.ctypes.data,
+                              ctypes.byref(secs)))
+    return (out, secs.value) if return_seconds else out
+
+
+def direct_mc(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, device: int = 0):
+    st = TrialStats()
+    _check(lib.mcb_direct_mc(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st)))
+    return st
+
+
+class Plan:
+    """Device-resident plan: descriptors and tile tables stay in HBM; ``launch``
+    enqueues the fused kernels on a CUDA stream (a ``torch.cuda.Stream``'s
+    ``cuda_stream`` handle or 0 for the legacy default stream)."""
+
+    def __init__(self, fns: Sequence[Integrand], seed: int, trials: int, device: int = 0):
+        self._arr = as_array(fns)
+        self.trials = trials
+        h = ctypes.c_void_p()
+        _check(lib.mcb_plan_create(self._arr, len(self._arr), seed, trials, device, ctypes.byref(h)))
+        self._h = h
+
+    def info(self) -> PlanInfo:
+        i = PlanInfo()
+        _check(lib.mcb_plan_get_info(self._h, ctypes.byref(i)))
+        return i
+
+    def launch(self, stream: int = 0) -> None:
+        _check(lib.mcb_plan_launch(self._h, ctypes.c_void_p(stream)))
+
+    def download(self, stream: int = 0) -> np.ndarray:
+        out = np.zeros((len(self._arr), self.trials), dtype=TRIAL_DTYPE)
+        _check(lib.mcb_plan_download(self._h, out.ctypes.data, ctypes.c_void_p(stream)))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.mcb_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def debug_points(seed: int, integrand_index: int, trial: int, chunk: int, first_point: int,
+                 count: int, low: Sequence[float], high: Sequence[float], device: int = 0):
+    dim = len(low)
+    out = np.zeros((count, dim), dtype=np.float64)
+    lo = (ctypes.c_double * dim)(*low)
+    hi = (ctypes.c_double * dim)(*high)
+    _check(lib.mcb_debug_points(seed, integrand_index, trial, chunk, first_point, count, dim, lo, hi,
+                                device, out.ctypes.data))
+    return out
+
+
+def debug_eval(f: Integrand, seed: int, trial: int, chunk: int, first_point: int, count: int,
+               device: int = 0):
+    out = np.zeros(count, dtype=np.float64)
+    _check(lib.mcb_debug_eval(ctypes.byref(f), seed, trial, chunk, first_point, count, device,
+                              out.ctypes.data))
+    return out
+
+
+def probe_mul_peak(device: int = 0, ms: float = 20.0) -> float:
+    v = ctypes.c_double()
+    _check(lib.mcb_probe_mul_peak(device, ms, ctypes.byref(v)))
+    return v.value
+
+
+from . import workloads  # noqa: E402,F401  (config builders)

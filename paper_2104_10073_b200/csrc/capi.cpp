@@ -1,0 +1,800 @@
+// capi.cpp — the C-ABI layer (include/mcb/mcb.h): validation, descriptor
+// lowering, device plans and the multi-GPU host scheduler.
+//
+// Reference correspondence (file:line under /root/reference/proj):
+//   mcb_validate        validate                 src/batch.cpp:62-120
+//   mcb_run_direct      run_batch (Direct)       src/batch.cpp:195-333
+//   mcb_direct_mc       direct_mc                src/estimator.cpp:75-92
+//   mcb_summarize_trials summarize_trials        src/estimator.cpp:320-337
+//   mcb_stream_key      UniformStream key        src/sampling.cpp:84-87
+//   mcb_volume          HyperRect::volume        src/sampling.cpp:16-20
+//   mcb_debug_points    sample_uniform           src/sampling.cpp:102-112
+// There is no CPU fallback: every numeric result comes from the sm_100a
+// kernels in direct.cu; without a device the compute entry points return
+// MCB_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "mcb/mcb.h"
+#include "mcb_internal.hpp"
+
+using mcb::detail::GroupLaunch;
+using mcb::dev::FnDesc;
+using mcb::dev::TilePartial;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+mcb_status fail(mcb_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+mcb_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(MCB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define MCB_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+uint64_t splitmix64(uint64_t z) {  // src/sampling.cpp:44-49
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+uint64_t chunk_count(uint64_t n) { return (n + MCB_CHUNK_SIZE - 1) / MCB_CHUNK_SIZE; }
+
+uint32_t min_dim(uint32_t family) {
+  return family == MCB_FAMILY_ABS2 ? 2u : (family == MCB_FAMILY_ABS3 ? 3u : 1u);
+}
+
+bool family_known(uint32_t f) { return f <= MCB_FAMILY_ABS3; }
+
+// Per-sample cost estimate (relative units) for LPT sharding: Philox blocks
+// dominate (d/2 per sample), a sincos costs about one block.
+double sample_cost(const mcb_integrand& f) {
+  double blocks = 0.5 * double(std::max(f.dim, 1u));
+  if (f.family == MCB_FAMILY_ABS2) blocks = std::min(blocks, 1.0);
+  if (f.family == MCB_FAMILY_ABS3) blocks = std::min(blocks, 1.5);
+  const bool harm = f.family == MCB_FAMILY_HARMONIC || f.family == MCB_FAMILY_HARMONIC_VEC;
+  return blocks + (harm ? 1.0 : 0.2);
+}
+
+// Reference-order evaluation on the host, used only for the shift constant
+// c = f(domain midpoint) (any finite c is correct; a c near the mean keeps
+// sum (f-c)^2 well conditioned, and for a constant f it makes the variance
+// exactly 0 as in the reference, tests/test_estimator.cpp:44-52).
+double host_eval(const mcb_integrand& f, const double* x) {
+  switch (f.family) {
+    case MCB_FAMILY_HARMONIC: {
+      double s = x[0];
+      for (uint32_t j = 1; j < f.dim; ++j) s = s + x[j];
+      const double t = f.k[0] * s;
+      if (f.flags & MCB_FLAG_UNIT_COEFFS) return std::cos(t) + std::sin(t);
+      const double c = f.a * std::cos(t), sn = f.b * std::sin(t);
+      return c + sn;
+    }
+    case MCB_FAMILY_HARMONIC_VEC: {
+      double t = f.k[0] * x[0];
+      for (uint32_t j = 1; j < f.dim; ++j) {
+        const double p = f.k[j] * x[j];
+        t = t + p;
+      }
+      const double c = f.a * std::cos(t), sn = f.b * std::sin(t);
+      return c + sn;
+    }
+    case MCB_FAMILY_ABS2:
+      return f.a * std::fabs(x[0] + x[1]);
+    case MCB_FAMILY_ABS3: {
+      const double s = x[0] + x[1];
+      return f.a * std::fabs(s - x[2]);
+    }
+  }
+  return 0.0;
+}
+
+void append_sum(std::string& s, uint32_t dim) {
+  for (uint32_t j = 0; j < dim; ++j) {
+    if (j) s += "+";
+    s += "x" + std::to_string(j + 1);
+  }
+}
+
+std::string to_dsl(const mcb_integrand& f) {
+  std::string s;
+  switch (f.family) {
+    case MCB_FAMILY_HARMONIC: {
+      std::string arg = "k*(";
+      append_sum(arg, f.dim);
+      arg += ")";
+      if (f.flags & MCB_FLAG_UNIT_COEFFS)
+        s = "cos(" + arg + ") + sin(" + arg + ")";  // src/job_io.cpp:367
+      else
+        s = "a*cos(" + arg + ") + b*sin(" + arg + ")";
+      break;
+    }
+    case MCB_FAMILY_HARMONIC_VEC: {
+      std::string arg;
+      for (uint32_t j = 0; j < f.dim; ++j) {
+        if (j) arg += "+";
+        arg += "k" + std::to_string(j + 1) + "*x" + std::to_string(j + 1);
+      }
+      s = "a*cos(" + arg + ") + b*sin(" + arg + ")";
+      break;
+    }
+    case MCB_FAMILY_ABS2:
+      s = f.a == 1.0 ? "abs(x1+x2)" : "a*abs(x1+x2)";  // tests/test_batch.cpp:49
+      break;
+    case MCB_FAMILY_ABS3:
+      s = f.a == 1.0 ? "abs(x1+x2-x3)" : "a*abs(x1+x2-x3)";  // tests/test_batch.cpp:51
+      break;
+    default:
+      s = "";
+  }
+  return s;
+}
+
+bool rect_valid(const mcb_integrand& f) {  // HyperRect::valid, src/sampling.cpp:7-14
+  if (f.dim < 1 || f.dim > MCB_MAX_DIM) return false;
+  for (uint32_t j = 0; j < f.dim; ++j) {
+    if (!(f.low[j] < f.high[j])) return false;
+    if (!std::isfinite(f.low[j]) || !std::isfinite(f.high[j])) return false;
+  }
+  return true;
+}
+
+double volume(const mcb_integrand& f) {  // src/sampling.cpp:16-20
+  double v = 1.0;
+  for (uint32_t j = 0; j < f.dim && j < MCB_MAX_DIM; ++j) v *= f.high[j] - f.low[j];
+  return v;
+}
+
+void violations_of(const mcb_integrand& f, uint32_t trials,
+                   std::vector<std::string>& out) {
+  if (!family_known(f.family)) {
+    out.push_back("unknown integrand family " + std::to_string(f.family));
+    return;
+  }
+  if (f.dim < 1) out.push_back("dim must be >= 1");
+  if (f.dim > MCB_MAX_DIM)
+    out.push_back("dim " + std::to_string(f.dim) + " exceeds the supported maximum " +
+                  std::to_string(MCB_MAX_DIM));
+  if (f.dim >= 1 && f.dim < min_dim(f.family))
+    out.push_back("x" + std::to_string(min_dim(f.family)) +
+                  " exceeds dim=" + std::to_string(f.dim));  // batch.cpp:102-105 wording
+  if (f.dim >= 1 && f.dim <= MCB_MAX_DIM && !rect_valid(f))
+    out.push_back("domain is invalid (need low[i] < high[i], finite, dim >= 1)");
+  if (f.n_samples < 2) out.push_back("samples must be >= 2");
+  if ((f.flags & MCB_FLAG_UNIT_COEFFS) &&
+      !(f.family == MCB_FAMILY_HARMONIC && f.a == 1.0 && f.b == 1.0))
+    out.push_back("unit-coefficient flag needs the harmonic family with a = b = 1");
+  if (f.flags & ~MCB_FLAG_UNIT_COEFFS) out.push_back("unknown flag bits");
+  const uint64_t nc = chunk_count(f.n_samples);
+  if (nc > 0xFFFFFFFFull) out.push_back("samples exceed 2^32 chunks (chunk_index is 32-bit)");
+  else if (nc * uint64_t(std::max(trials, 1u)) > 0xFFFFFFFFull)
+    out.push_back("chunks x trials exceeds 2^32 work units for one integrand");
+}
+
+// ---- variant selection -----------------------------------------------------
+
+constexpr double kTwoM64 = 0x1p-64;
+constexpr double kMinFold = 0x1p-958;  // |p| * 2^-64 stays a normal double
+
+bool foldable(double p) { return p == 0.0 || std::fabs(p) >= kMinFold; }
+
+struct Prepared {
+  FnDesc d;
+  int variant;
+};
+
+// Decide the kernel variant and fill the device descriptor.  FAST variants
+// need (host-proven, for every point of the domain): finite parameters,
+// |t| < 2^30 for the sincos reduction, no overflow of f, and exact 2^-64
+// folding.  Anything else runs the SAFE variant (libdevice sincos, counted
+// non-finite samples) — still on the GPU.
+Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
+                 uint32_t trial_base) {
+  using namespace mcb::detail;
+  Prepared p;
+  FnDesc& d = p.d;
+  std::memset(&d, 0, sizeof d);
+  uint32_t key[2];
+  mcb_stream_key(seed, f.integrand_index, key);
+  d.key0 = key[0];
+  d.key1 = key[1];
+  d.n_chunks = uint32_t(chunk_count(f.n_samples));
+  d.chunk_base = chunk_base;
+  d.trial_base = trial_base;
+  d.n_samples = f.n_samples;
+  d.a = f.a;
+  d.b = f.b;
+  d.volume = volume(f);
+  bool unit_dom = true;
+  double xmax = 0.0;  // bound on sum_j |x_j| (or |k_j x_j|)
+  bool finite = std::isfinite(f.a) && std::isfinite(f.b);
+  for (uint32_t j = 0; j < f.dim; ++j) {
+    d.low[j] = f.low[j];
+    d.width[j] = f.high[j] - f.low[j];
+    d.k[j] = f.k[j];
+    if (!(f.low[j] == 0.0 && f.high[j] == 1.0)) unit_dom = false;
+    const double m = std::max(std::fabs(f.low[j]), std::fabs(f.high[j]));
+    if (f.family == MCB_FAMILY_HARMONIC_VEC) {
+      finite = finite && std::isfinite(f.k[j]);
+      xmax += std::fabs(f.k[j]) * m;
+    } else {
+      xmax += m;
+    }
+  }
+  if (f.family == MCB_FAMILY_HARMONIC) finite = finite && std::isfinite(f.k[0]);
+  const bool unit_coef = (f.flags & MCB_FLAG_UNIT_COEFFS) != 0;
+  const bool harm = f.family == MCB_FAMILY_HARMONIC || f.family == MCB_FAMILY_HARMONIC_VEC;
+
+  bool fast = finite && std::isfinite(xmax);
+  if (fast && harm) {
+    const double tmax = f.family == MCB_FAMILY_HARMONIC ? std::fabs(f.k[0]) * xmax * 1.0000001
+                                                        : xmax * 1.0000001;
+    fast = tmax < 0x1p30 && std::fabs(f.a) + std::fabs(f.b) < 1e300;
+  }
+  if (fast && !harm) fast = std::fabs(f.a) * xmax < 1e300;
+  // 2^-64 folding: onto the factor that multiplies the raw draw
+  if (fast) {
+    if (unit_dom) {
+      if (f.family == MCB_FAMILY_HARMONIC) fast = foldable(f.k[0]);
+      else if (f.family == MCB_FAMILY_HARMONIC_VEC)
+        for (uint32_t j = 0; j < f.dim; ++j) fast = fast && foldable(f.k[j]);
+      else fast = foldable(f.a);
+    } else {
+      for (uint32_t j = 0; j < f.dim; ++j) fast = fast && foldable(d.width[j]);
+    }
+  }
+  if (fast) {
+    if (unit_dom) {
+      if (f.family == MCB_FAMILY_HARMONIC) d.k[0] = f.k[0] * kTwoM64;
+      else if (f.family == MCB_FAMILY_HARMONIC_VEC)
+        for (uint32_t j = 0; j < f.dim; ++j) d.k[j] = f.k[j] * kTwoM64;
+      else d.a = f.a * kTwoM64;
+    } else {
+      for (uint32_t j = 0; j < f.dim; ++j) d.width[j] = d.width[j] * kTwoM64;
+    }
+    p.variant = (unit_dom ? kUnitDomain : 0) | (unit_coef ? kUnitCoef : 0);
+  } else {
+    p.variant = kSafe;
+  }
+  if (!harm) p.variant &= ~kUnitCoef;
+  // shift constant: f at the domain midpoint (reference op order, libm)
+  double mid[MCB_MAX_DIM];
+  for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
+  const double c = host_eval(f, mid);
+  d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
+  return p;
+}
+
+}  // namespace
+
+// ---- plans -------------------------------------------------------------------
+
+struct mcb_plan {
+  int device = 0;
+  uint64_t n_fns = 0;
+  uint32_t trials = 0;
+  uint64_t n_tiles = 0;
+  uint64_t total_samples = 0;
+  uint64_t philox_blocks = 0;
+  std::vector<GroupLaunch> groups;
+  FnDesc* d_fns = nullptr;
+  uint32_t* d_tile_fn = nullptr;
+  TilePartial* d_part = nullptr;
+  mcb_trial_stats* d_out = nullptr;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+mcb_status check_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(MCB_ERR_NO_DEVICE, "no CUDA device visible (the mcb path has no CPU fallback)");
+  if (device < 0 || device >= n)
+    return fail(MCB_ERR_INVALID_ARGUMENT, "device ordinal " + std::to_string(device) +
+                                              " out of range (" + std::to_string(n) + " visible)");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return fail(MCB_ERR_NO_DEVICE, "cannot query device");
+  if (prop.major != 10)
+    return fail(MCB_ERR_NO_DEVICE, std::string("device ") + prop.name +
+                                       " is not sm_100 (this build targets sm_100a only)");
+  return MCB_OK;
+}
+
+mcb_status validate_for_run(const mcb_integrand* fns, size_t n_fns, uint32_t trials) {
+  if (!fns && n_fns) return fail(MCB_ERR_INVALID_ARGUMENT, "fns is NULL");
+  std::vector<mcb_violation> v(16);
+  size_t n = 0;
+  mcb_validate(fns, n_fns, nullptr, trials, v.data(), v.size(), &n);
+  if (n == 0) return MCB_OK;
+  std::string msg = "job validation failed (" + std::to_string(n) + " problem(s)):";
+  for (size_t i = 0; i < std::min(n, v.size()); ++i) {
+    msg += "\n  ";
+    if (v[i].integrand >= 0) msg += "f" + std::to_string(v[i].integrand) + ": ";
+    msg += v[i].message;
+  }
+  return fail(MCB_ERR_VALIDATION, msg);
+}
+
+mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
+                            uint32_t trials, int device, uint32_t chunk_base,
+                            uint32_t trial_base, mcb_plan** out) {
+  mcb_status st = validate_for_run(fns, n_fns, trials);
+  if (st != MCB_OK) return st;
+  if (chunk_base) {
+    for (size_t i = 0; i < n_fns; ++i)
+      if (uint64_t(chunk_base) + chunk_count(fns[i].n_samples) - 1 > 0xFFFFFFFFull)
+        return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
+  }
+  if ((st = check_device(device)) != MCB_OK) return st;
+
+  std::vector<Prepared> prep(n_fns);
+  for (size_t i = 0; i < n_fns; ++i) prep[i] = prepare(fns[i], seed, chunk_base, trial_base);
+  // groups: (family, dim, variant), stable in job order
+  std::vector<size_t> order(n_fns);
+  std::iota(order.begin(), order.end(), size_t(0));
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+    auto kx = std::make_tuple(fns[x].family, fns[x].dim, prep[x].variant);
+    auto ky = std::make_tuple(fns[y].family, fns[y].dim, prep[y].variant);
+    return kx < ky;
+  });
+  auto plan = new mcb_plan();
+  plan->device = device;
+  plan->n_fns = n_fns;
+  plan->trials = trials;
+  std::vector<FnDesc> host(n_fns);
+  uint64_t tile = 0;
+  for (size_t r = 0; r < n_fns; ++r) {
+    const size_t i = order[r];
+    FnDesc d = prep[i].d;
+    d.tile_base = tile;
+    d.out_slot = i;
+    const uint64_t nt = uint64_t(d.n_chunks) * trials;
+    const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
+    if (plan->groups.empty() || plan->groups.back().family != fam ||
+        plan->groups.back().dim != dim || plan->groups.back().variant != var)
+      plan->groups.push_back(GroupLaunch{fam, dim, var, tile, 0});
+    plan->groups.back().n_tiles += nt;
+    tile += nt;
+    host[r] = d;
+    plan->total_samples += fns[i].n_samples * trials;
+    // Philox blocks per chunk: pairs * dim (blocks of unused ABS coordinates skipped)
+    const uint64_t used_dim = fam == MCB_FAMILY_ABS2   ? std::min<uint32_t>(dim, 2)
+                              : fam == MCB_FAMILY_ABS3 ? std::min<uint32_t>(dim, 3)
+                                                       : uint64_t(dim);
+    (void)used_dim;
+    const uint64_t full = fns[i].n_samples / MCB_CHUNK_SIZE, last = fns[i].n_samples % MCB_CHUNK_SIZE;
+    const uint64_t blocks_per_fn_trial =
+        full * (MCB_CHUNK_SIZE / 2) * uint64_t(dim) + ((last + 1) / 2) * uint64_t(dim);
+    plan->philox_blocks += blocks_per_fn_trial * trials;
+  }
+  for (const auto& g : plan->groups)
+    if (!mcb::detail::variant_supported(g.family, g.dim, g.variant)) {
+      delete plan;
+      return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
+    }
+  plan->n_tiles = tile;
+
+  DeviceGuard guard(device);
+  auto cleanup = [&](cudaError_t e, const char* what) {
+    mcb_plan_destroy(plan);
+    return cuda_fail(e, what);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&plan->d_fns, sizeof(FnDesc) * std::max<size_t>(n_fns, 1))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc(fns)");
+  if ((e = cudaMalloc(&plan->d_tile_fn, sizeof(uint32_t) * std::max<uint64_t>(tile, 1))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc(tile_fn)");
+  if ((e = cudaMalloc(&plan->d_part, sizeof(TilePartial) * std::max<uint64_t>(tile, 1))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc(partials)");
+  if ((e = cudaMalloc(&plan->d_out, sizeof(mcb_trial_stats) * std::max<uint64_t>(n_fns * trials, 1))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc(out)");
+  if ((e = cudaMemcpy(plan->d_fns, host.data(), sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cleanup(e, "cudaMemcpy(fns)");
+  if ((e = mcb::detail::launch_expand_tiles(plan->d_fns, uint32_t(n_fns), trials, plan->d_tile_fn, 0)) != cudaSuccess)
+    return cleanup(e, "expand_tiles");
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(e, "cudaDeviceSynchronize");
+  *out = plan;
+  return MCB_OK;
+}
+
+mcb_status plan_launch_impl(mcb_plan* plan, cudaStream_t s) {
+  DeviceGuard guard(plan->device);
+  for (const auto& g : plan->groups) {
+    cudaError_t e = mcb::detail::launch_direct_group(g, plan->d_fns, plan->d_tile_fn, plan->d_part, s);
+    if (e != cudaSuccess) return cuda_fail(e, "launch k_direct");
+  }
+  cudaError_t e = mcb::detail::launch_combine(plan->d_fns, uint32_t(plan->n_fns), plan->trials,
+                                              plan->d_part, plan->d_out, s);
+  if (e != cudaSuccess) return cuda_fail(e, "launch k_combine");
+  return MCB_OK;
+}
+
+mcb_status plan_download_impl(mcb_plan* plan, mcb_trial_stats* out, cudaStream_t s) {
+  DeviceGuard guard(plan->device);
+  MCB_CUDA(cudaMemcpyAsync(out, plan->d_out, sizeof(mcb_trial_stats) * plan->n_fns * plan->trials,
+                           cudaMemcpyDeviceToHost, s));
+  MCB_CUDA(cudaStreamSynchronize(s));
+  return MCB_OK;
+}
+
+// LPT: integrands by decreasing cost onto the least-loaded shard.
+void lpt(const mcb_integrand* fns, size_t n, uint32_t trials, int shards, uint32_t* shard_of) {
+  std::vector<size_t> order(n);
+  std::iota(order.begin(), order.end(), size_t(0));
+  std::vector<double> cost(n);
+  for (size_t i = 0; i < n; ++i)
+    cost[i] = double(fns[i].n_samples) * double(trials) * sample_cost(fns[i]);
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
+  std::vector<double> load(size_t(shards), 0.0);
+  for (size_t i : order) {
+    size_t best = 0;
+    for (size_t s = 1; s < load.size(); ++s)
+      if (load[s] < load[best]) best = s;
+    shard_of[i] = uint32_t(best);
+    load[best] += cost[i];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t mcb_abi_version(void) { return MCB_ABI_VERSION; }
+
+const char* mcb_last_error(void) { return g_last_error.c_str(); }
+
+int mcb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void mcb_stream_key(uint64_t global_seed, uint32_t integrand_index, uint32_t key_out[2]) {
+  uint64_t h = splitmix64(global_seed);
+  h = splitmix64(h ^ (0x9E3779B97F4A7C15ull * (uint64_t(integrand_index) + 1)));
+  key_out[0] = uint32_t(h);
+  key_out[1] = uint32_t(h >> 32);
+}
+
+double mcb_volume(const mcb_integrand* fn) { return fn ? volume(*fn) : 0.0; }
+
+size_t mcb_to_dsl(const mcb_integrand* fn, char* buf, size_t cap) {
+  if (!fn) return 0;
+  const std::string s = to_dsl(*fn);
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return s.size() + 1;
+}
+
+mcb_status mcb_validate(const mcb_integrand* fns, size_t n_fns, const char* const* names,
+                        uint32_t trials, mcb_violation* out, size_t cap, size_t* n_out) {
+  std::vector<std::pair<int64_t, std::string>> v;
+  if (trials < 1) v.push_back({-1, "trials must be >= 1"});
+  if (n_fns == 0) v.push_back({-1, "integrand list is empty"});
+  if (n_fns && !fns) return fail(MCB_ERR_INVALID_ARGUMENT, "fns is NULL");
+  std::map<std::string, int> name_count;
+  if (names)
+    for (size_t i = 0; i < n_fns; ++i) ++name_count[names[i] ? names[i] : ""];
+  for (size_t i = 0; i < n_fns; ++i) {
+    std::vector<std::string> msgs;
+    if (names && (!names[i] || !names[i][0])) msgs.push_back("integrand name is empty");
+    violations_of(fns[i], trials, msgs);
+    for (auto& m : msgs) v.push_back({int64_t(i), m});
+  }
+  if (names)  // duplicate names, once per offending name (src/batch.cpp:113-118)
+    for (const auto& [name, count] : name_count)
+      if (count > 1) {
+        int64_t first = -1;
+        for (size_t i = 0; i < n_fns; ++i)
+          if (names[i] && name == names[i]) { first = int64_t(i); break; }
+        v.push_back({first, "duplicate integrand name (" + std::to_string(count) + " occurrences)"});
+      }
+  if (n_out) *n_out = v.size();
+  for (size_t i = 0; i < v.size() && i < cap && out; ++i) {
+    out[i].integrand = v[i].first;
+    std::snprintf(out[i].message, sizeof out[i].message, "%s", v[i].second.c_str());
+  }
+  return MCB_OK;
+}
+
+mcb_status mcb_partition(const mcb_integrand* fns, size_t n_fns, uint32_t trials, int n_shards,
+                         uint32_t* shard_of_fn) {
+  if (n_shards < 1) return fail(MCB_ERR_INVALID_ARGUMENT, "n_shards must be >= 1");
+  if (n_fns && (!fns || !shard_of_fn)) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL buffer");
+  lpt(fns, n_fns, trials, n_shards, shard_of_fn);
+  return MCB_OK;
+}
+
+mcb_status mcb_summarize_trials(const mcb_trial_stats* per_trial, uint32_t n_trials, double* mean,
+                                double* trial_stddev, uint32_t* n_ok) {
+  if (!per_trial || !mean || !trial_stddev) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL buffer");
+  double sum = 0.0;
+  uint32_t r = 0;
+  for (uint32_t t = 0; t < n_trials; ++t)
+    if (per_trial[t].status == MCB_TRIAL_OK) {
+      sum += per_trial[t].value;
+      ++r;
+    }
+  if (n_ok) *n_ok = r;
+  if (r == 0) return fail(MCB_ERR_INVALID_ARGUMENT, "no successful trials");  // InsufficientTrials
+  *mean = sum / double(r);
+  *trial_stddev = 0.0;
+  if (r >= 2) {
+    double ss = 0.0;
+    for (uint32_t t = 0; t < n_trials; ++t)
+      if (per_trial[t].status == MCB_TRIAL_OK) {
+        const double d = per_trial[t].value - *mean;
+        ss += d * d;
+      }
+    *trial_stddev = std::sqrt(ss / double(r - 1));
+  }
+  return MCB_OK;
+}
+
+mcb_status mcb_plan_create(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
+                           int device, mcb_plan** plan_out) {
+  if (!plan_out) return fail(MCB_ERR_INVALID_ARGUMENT, "plan_out is NULL");
+  *plan_out = nullptr;
+  return plan_create_impl(fns, n_fns, seed, trials, device, 0, 0, plan_out);
+}
+
+mcb_status mcb_plan_launch(mcb_plan* plan, void* stream) {
+  if (!plan) return fail(MCB_ERR_INVALID_ARGUMENT, "plan is NULL");
+  return plan_launch_impl(plan, static_cast<cudaStream_t>(stream));
+}
+
+mcb_status mcb_plan_download(mcb_plan* plan, mcb_trial_stats* out, void* stream) {
+  if (!plan || !out) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  return plan_download_impl(plan, out, static_cast<cudaStream_t>(stream));
+}
+
+mcb_status mcb_plan_get_info(const mcb_plan* plan, mcb_plan_info* info) {
+  if (!plan || !info) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  std::memset(info, 0, sizeof *info);
+  info->n_fns = plan->n_fns;
+  info->trials = plan->trials;
+  info->n_groups = uint32_t(plan->groups.size());
+  info->n_tiles = plan->n_tiles;
+  info->total_samples = plan->total_samples;
+  info->philox_blocks = plan->philox_blocks;
+  uint32_t launches = 1;  // k_combine
+  for (const auto& g : plan->groups) launches += uint32_t((g.n_tiles + 0x7FFFFFFEull) / 0x7FFFFFFFull);
+  info->launches_per_run = launches;
+  return MCB_OK;
+}
+
+void mcb_plan_destroy(mcb_plan* plan) {
+  if (!plan) return;
+  {
+    DeviceGuard guard(plan->device);
+    if (plan->d_fns) cudaFree(plan->d_fns);
+    if (plan->d_tile_fn) cudaFree(plan->d_tile_fn);
+    if (plan->d_part) cudaFree(plan->d_part);
+    if (plan->d_out) cudaFree(plan->d_out);
+  }
+  delete plan;
+}
+
+mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
+                          const int* devices, int n_devices, mcb_trial_stats* out,
+                          double* seconds) {
+  mcb_status st = validate_for_run(fns, n_fns, trials);
+  if (st != MCB_OK) return st;
+  if (!out) return fail(MCB_ERR_INVALID_ARGUMENT, "out is NULL");
+  std::vector<int> devs;
+  if (!devices || n_devices <= 0) devs.push_back(0);
+  else devs.assign(devices, devices + n_devices);
+  for (int d : devs)
+    if ((st = check_device(d)) != MCB_OK) return st;
+
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<uint32_t> shard(n_fns, 0);
+  lpt(fns, n_fns, trials, int(devs.size()), shard.data());
+  std::vector<mcb_status> status(devs.size(), MCB_OK);
+  std::vector<std::string> errors(devs.size());
+  auto work = [&](size_t w) {
+    std::vector<size_t> mine;
+    for (size_t i = 0; i < n_fns; ++i)
+      if (shard[i] == w) mine.push_back(i);
+    if (mine.empty()) return;
+    std::vector<mcb_integrand> sub(mine.size());
+    for (size_t r = 0; r < mine.size(); ++r) sub[r] = fns[mine[r]];
+    mcb_plan* plan = nullptr;
+    mcb_status s = plan_create_impl(sub.data(), sub.size(), seed, trials, devs[w], 0, 0, &plan);
+    std::vector<mcb_trial_stats> res(sub.size() * trials);
+    cudaStream_t stream = nullptr;
+    if (s == MCB_OK) {
+      DeviceGuard guard(devs[w]);
+      if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess)
+        s = fail(MCB_ERR_CUDA, "cudaStreamCreate failed");
+    }
+    if (s == MCB_OK) s = plan_launch_impl(plan, stream);
+    if (s == MCB_OK) s = plan_download_impl(plan, res.data(), stream);
+    if (stream) {
+      DeviceGuard guard(devs[w]);
+      cudaStreamDestroy(stream);
+    }
+    mcb_plan_destroy(plan);
+    status[w] = s;
+    if (s != MCB_OK) {
+      errors[w] = g_last_error;
+      return;
+    }
+    for (size_t r = 0; r < mine.size(); ++r)
+      std::memcpy(out + mine[r] * trials, res.data() + r * trials, sizeof(mcb_trial_stats) * trials);
+  };
+  if (devs.size() == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (size_t w = 0; w < devs.size(); ++w) pool.emplace_back(work, w);
+    for (auto& th : pool) th.join();
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+  for (size_t w = 0; w < devs.size(); ++w)
+    if (status[w] != MCB_OK) return fail(status[w], "device " + std::to_string(devs[w]) + ": " + errors[w]);
+  return MCB_OK;
+}
+
+mcb_status mcb_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial, uint64_t chunk_base,
+                         int device, mcb_trial_stats* out) {
+  if (!fn || !out) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (fn->n_samples < 2) return fail(MCB_ERR_INVALID_ARGUMENT, "n_samples must be >= 2");
+  if (chunk_base + chunk_count(fn->n_samples) - 1 > 0xFFFFFFFFull)
+    return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
+  // One (integrand, trial) unit: a 1-trial plan whose key base is
+  // {seed, integrand_index, trial, chunk_base}.
+  mcb_plan* plan = nullptr;
+  mcb_status st = plan_create_impl(fn, 1, seed, 1, device, uint32_t(chunk_base), trial, &plan);
+  if (st != MCB_OK) return st;
+  st = plan_launch_impl(plan, nullptr);
+  if (st == MCB_OK) st = plan_download_impl(plan, out, nullptr);
+  mcb_plan_destroy(plan);
+  return st;
+}
+
+mcb_status mcb_debug_points(uint64_t seed, uint32_t integrand_index, uint32_t trial, uint64_t chunk,
+                            uint64_t first_point, uint64_t count, uint32_t dim, const double* low,
+                            const double* high, int device, double* out) {
+  if (dim < 1 || dim > MCB_MAX_DIM || !low || !high || (count && !out))
+    return fail(MCB_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (chunk > 0xFFFFFFFFull) return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
+  if ((first_point + count) * dim / 2 > 0xFFFFFFFFull)
+    return fail(MCB_ERR_OUT_OF_RANGE, "block index exceeds 32 bits");
+  mcb_status st = check_device(device);
+  if (st != MCB_OK) return st;
+  if (count == 0) return MCB_OK;
+  DeviceGuard guard(device);
+  uint32_t key[2];
+  mcb_stream_key(seed, integrand_index, key);
+  double hw[2 * MCB_MAX_DIM];
+  for (uint32_t j = 0; j < dim; ++j) {
+    hw[j] = low[j];
+    hw[MCB_MAX_DIM + j] = high[j] - low[j];
+  }
+  double* d_lw = nullptr;
+  double* d_out = nullptr;
+  MCB_CUDA(cudaMalloc(&d_lw, sizeof hw));
+  cudaError_t e = cudaMalloc(&d_out, sizeof(double) * count * dim);
+  if (e == cudaSuccess) e = cudaMemcpy(d_lw, hw, sizeof hw, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = mcb::detail::launch_debug_points(key[0], key[1], trial, uint32_t(chunk), first_point, count,
+                                         dim, d_lw, d_lw + MCB_MAX_DIM, d_out, nullptr);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(out, d_out, sizeof(double) * count * dim, cudaMemcpyDeviceToHost);
+  cudaFree(d_lw);
+  if (d_out) cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_fail(e, "debug_points");
+  return MCB_OK;
+}
+
+mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial, uint64_t chunk,
+                          uint64_t first_point, uint64_t count, int device, double* out) {
+  if (!fn || (count && !out)) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  std::vector<std::string> msgs;
+  violations_of(*fn, 1, msgs);
+  if (!msgs.empty()) return fail(MCB_ERR_VALIDATION, msgs.front());
+  if (chunk > 0xFFFFFFFFull) return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
+  if (first_point + count > MCB_CHUNK_SIZE)
+    return fail(MCB_ERR_OUT_OF_RANGE, "points must lie inside one chunk");
+  mcb_status st = check_device(device);
+  if (st != MCB_OK) return st;
+  if (count == 0) return MCB_OK;
+  DeviceGuard guard(device);
+  const Prepared p = prepare(*fn, seed, 0, 0);
+  const uint64_t first_pair = first_point / 2;
+  const uint64_t n_pairs = (first_point + count - 1) / 2 - first_pair + 1;
+  FnDesc* d_fn = nullptr;
+  double* d_out = nullptr;
+  MCB_CUDA(cudaMalloc(&d_fn, sizeof(FnDesc)));
+  cudaError_t e = cudaMalloc(&d_out, sizeof(double) * 2 * n_pairs);
+  if (e == cudaSuccess) e = cudaMemcpy(d_fn, &p.d, sizeof(FnDesc), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = mcb::detail::launch_debug_eval_impl(int(fn->family), int(fn->dim), p.variant, d_fn, trial,
+                                            uint32_t(chunk), uint32_t(first_pair), uint32_t(n_pairs),
+                                            d_out, nullptr);
+  std::vector<double> tmp(2 * n_pairs);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(tmp.data(), d_out, sizeof(double) * 2 * n_pairs, cudaMemcpyDeviceToHost);
+  cudaFree(d_fn);
+  if (d_out) cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_fail(e, "debug_eval");
+  std::memcpy(out, tmp.data() + (first_point - 2 * first_pair), sizeof(double) * count);
+  return MCB_OK;
+}
+
+mcb_status mcb_probe_mul_peak(int device, double ms, double* muls_per_s) {
+  if (!muls_per_s) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  mcb_status st = check_device(device);
+  if (st != MCB_OK) return st;
+  DeviceGuard guard(device);
+  cudaDeviceProp prop;
+  MCB_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int ctas = prop.multiProcessorCount * 8;
+  uint32_t* sink = nullptr;
+  MCB_CUDA(cudaMalloc(&sink, sizeof(uint32_t) * ctas));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  int iters = 1024;
+  float elapsed = 0.f;
+  cudaError_t e = cudaSuccess;
+  for (int round = 0; round < 12; ++round) {  // grow until the launch takes ~ms
+    cudaEventRecord(a);
+    e = mcb::detail::launch_mul_probe(sink, ctas, iters, nullptr);
+    cudaEventRecord(b);
+    if (e == cudaSuccess) e = cudaEventSynchronize(b);
+    if (e != cudaSuccess) break;
+    cudaEventElapsedTime(&elapsed, a, b);
+    if (elapsed >= ms) break;
+    iters *= 2;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  if (e != cudaSuccess) return cuda_fail(e, "mul_probe");
+  *muls_per_s = double(ctas) * 256.0 * 8.0 * double(iters) / (double(elapsed) * 1e-3);
+  return MCB_OK;
+}
+
+}  // extern "C"

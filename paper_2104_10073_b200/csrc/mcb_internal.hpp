@@ -1,0 +1,53 @@
+// mcb_internal.hpp — host-side declarations shared by the C-ABI layer and the
+// CUDA translation unit.  Not part of the public interface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "mcb/mcb.h"
+#include "mcb_device.cuh"
+
+namespace mcb {
+namespace detail {
+
+constexpr int kThreads = 256;  // CTA size of the fused kernel (8 warps)
+
+enum Variant : int {
+  kUnitDomain = 1,  // low == 0, width == 1 on every axis
+  kUnitCoef = 2,    // HARMONIC with a == b == 1 (Fig.1 source form)
+  kSafe = 4         // plain parameters, libdevice sincos, non-finite samples
+                    // counted and skipped (used when the host cannot prove
+                    // the FAST preconditions, see capi.cpp choose_variant)
+};
+
+// One kernel launch = one (family, dim, variant) group of integrands whose
+// tiles are contiguous in the plan's tile space.
+struct GroupLaunch {
+  int family, dim, variant;
+  uint64_t tile0, n_tiles;
+};
+
+bool variant_supported(int family, int dim, int variant);
+
+cudaError_t launch_direct_group(const GroupLaunch& g, const dev::FnDesc* fns,
+                                const uint32_t* tile_fn, dev::TilePartial* part,
+                                cudaStream_t s);
+cudaError_t launch_expand_tiles(const dev::FnDesc* fns, uint32_t n_fns, uint32_t trials,
+                                uint32_t* tile_fn, cudaStream_t s);
+cudaError_t launch_combine(const dev::FnDesc* fns, uint32_t n_fns, uint32_t trials,
+                           const dev::TilePartial* part, mcb_trial_stats* out,
+                           cudaStream_t s);
+cudaError_t launch_debug_points(uint32_t key0, uint32_t key1, uint32_t trial, uint32_t chunk,
+                                uint64_t first_point, uint64_t count, uint32_t dim,
+                                const double* low, const double* width, double* out,
+                                cudaStream_t s);
+cudaError_t launch_debug_eval_impl(int family, int dim, int variant, const dev::FnDesc* fn,
+                                   uint32_t trial, uint32_t chunk, uint32_t first_pair,
+                                   uint32_t n_pairs, double* out, cudaStream_t s);
+cudaError_t launch_mul_probe(uint32_t* sink, int n_ctas, int iters, cudaStream_t s);
+
+}  // namespace detail
+}  // namespace mcb

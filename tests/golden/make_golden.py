@@ -1,0 +1,163 @@
+"""Generate golden vectors from the REFERENCE ITSELF.
+
+Runs in the build container only: it needs oracle/_ref/libmcbatch_ref.so,
+which `make -C oracle ref` compiles from the unmodified reference sources
+under /root/reference/proj (src/{expr,sampling,estimator,batch,job_io}.cpp).
+Every number in golden.json is produced by the reference's own functions:
+  sample_uniform   src/sampling.cpp:102-112
+  evaluate         src/expr.cpp:520-553 (on the mcb_to_dsl source)
+  direct_mc        src/estimator.cpp:75-92
+  run_batch        src/batch.cpp:195-333
+  make_harmonic_job / harmonic_closed_form   src/job_io.cpp:336-376
+Doubles are stored as float.hex() strings so comparisons are bit-exact.
+
+    python tests/golden/make_golden.py      # rewrites tests/golden/golden.json
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+import paper_2104_10073_b200 as mcb  # noqa: E402  (descriptor structs + mcb_to_dsl only)
+from paper_2104_10073_b200 import workloads  # noqa: E402
+from tests import _oracle  # noqa: E402
+
+H = float.hex
+
+
+def desc_json(f):
+    return {"family": f.family, "dim": f.dim, "integrand_index": f.integrand_index,
+            "flags": f.flags, "n_samples": f.n_samples, "a": H(f.a), "b": H(f.b),
+            "k": [H(f.k[j]) for j in range(8)], "low": [H(f.low[j]) for j in range(8)],
+            "high": [H(f.high[j]) for j in range(8)], "source": mcb.to_dsl(f)}
+
+
+def stats_json(st):
+    return {"value": H(st.value), "std_error": H(st.std_error), "n_samples": int(st.n_samples),
+            "n_nonfinite": int(st.n_nonfinite), "status": int(st.status),
+            "nonfinite_warning": int(st.nonfinite_warning)}
+
+
+def ref_points(ref, low, high, seed, integrand, trial, chunk, count):
+    d = len(low)
+    out = np.zeros(count * d)
+    rc = ref.ref_sample_uniform(d, (ctypes.c_double * d)(*low), (ctypes.c_double * d)(*high), seed,
+                                integrand, trial, chunk, count, out.ctypes.data)
+    assert rc == 0, ref.ref_last_error()
+    return out.reshape(count, d)
+
+
+def main():
+    ref = _oracle.load_ref()
+    if ref is None:
+        sys.exit("oracle/_ref/libmcbatch_ref.so missing: run `make -C oracle ref` first")
+    g = {"generator": "tests/golden/make_golden.py (reference compiled from /root/reference/proj)"}
+
+    # 1. points, including odd-d block straddling, chunk/trial > 0, non-unit domains
+    pts_cases = []
+    rng = np.random.default_rng(7)
+    specs = [(20200814, 0, 0, 0, [0.0] * 4, [1.0] * 4, 8),
+             (20200814, 99, 9, 15, [0.0] * 4, [1.0] * 4, 3),
+             (7, 1, 0, 0, [0.0] * 3, [1.0] * 3, 5),
+             (0, 0, 0, 0, [0.0], [1.0], 6),
+             (123, 4, 5, 6, [-1.5, 10.0], [2.25, 20.0], 9),
+             (99, 3, 2, 1, [5.0], [5.0 + 1e-6], 7)]
+    for d in range(1, 9):
+        lo = list(rng.uniform(-3, 0, d))
+        hi = [x + w for x, w in zip(lo, rng.uniform(0.5, 4, d))]
+        specs.append((int(rng.integers(0, 2**63)), int(rng.integers(0, 5000)), int(rng.integers(0, 10)),
+                      int(rng.integers(0, 200)), lo, hi, 11))
+    for seed, i, t, c, lo, hi, n in specs:
+        p = ref_points(ref, lo, hi, seed, i, t, c, n)
+        pts_cases.append({"seed": seed, "integrand": i, "trial": t, "chunk": c,
+                          "low": [H(x) for x in lo], "high": [H(x) for x in hi],
+                          "points": [[H(x) for x in row] for row in p]})
+    g["points"] = pts_cases
+
+    # 2. family values on reference points (evaluate on the lowered source)
+    fam = [mcb.harmonic(workloads.harmonic_k(1), 4, unit_coeffs=True),
+           mcb.harmonic(3.7, 3, a=0.5, b=-2.0, low=[-1, 0, 2], high=[1, 0.5, 3]),
+           mcb.make_integrand(mcb.FAMILY_HARMONIC_VEC, 5, k=[1.5, -2.0, 0.25, 7.0, 3.0], a=1.25,
+                              b=0.75),
+           mcb.make_integrand(mcb.FAMILY_ABS2, 2, a=1.0),
+           mcb.make_integrand(mcb.FAMILY_ABS2, 2, a=1.3, low=[-0.4, 0.0], high=[1.0, 1.4]),
+           mcb.make_integrand(mcb.FAMILY_ABS3, 3, a=0.8, low=[0, -0.25, 0], high=[1, 1, 1.5]),
+           mcb.harmonic(workloads.harmonic_k(100), 7, unit_coeffs=True)]
+    ev = []
+    for idx, f in enumerate(fam):
+        f.integrand_index = idx
+        p = ref_points(ref, [f.low[j] for j in range(f.dim)], [f.high[j] for j in range(f.dim)],
+                       20200814, idx, 1, 2, 64)
+        vals = np.zeros(64)
+        rc = ref.ref_eval_points(mcb.to_dsl(f).encode(), ctypes.byref(f), p.ctypes.data, 64,
+                                 vals.ctypes.data)
+        assert rc == 0, ref.ref_last_error()
+        ev.append({"desc": desc_json(f), "seed": 20200814, "trial": 1, "chunk": 2,
+                   "values": [H(v) for v in vals]})
+    g["evals"] = ev
+
+    # 3. direct_mc estimates (partial last chunk, chunk_base, trial > 0)
+    dm = []
+    cases = [(mcb.harmonic(workloads.harmonic_k(1), 4, unit_coeffs=True, n_samples=1_000_000), 20200814, 0, 0),
+             (mcb.harmonic(workloads.harmonic_k(100), 4, unit_coeffs=True, n_samples=1_000_000, index=99), 20200814, 9, 0),
+             (mcb.harmonic(51.0 / (2 * np.pi), 4, unit_coeffs=True, n_samples=1_000_000), 77, 0, 0),
+             (mcb.make_integrand(mcb.FAMILY_ABS2, 2, n_samples=1_000_000), 3, 0, 0),
+             (mcb.make_integrand(mcb.FAMILY_ABS3, 3, a=1.0, n_samples=150_001, index=4), 11, 3, 5),
+             (mcb.harmonic(0.0, 2, a=7.0, b=1.0, low=[0, 0], high=[2, 2], n_samples=1000, index=2), 1, 0, 0),
+             (mcb.harmonic(2.5, 6, a=1.5, b=0.5, low=[-0.5] * 6, high=[0.75] * 6, n_samples=200_003, index=17), 5, 2, 3),
+             (mcb.make_integrand(mcb.FAMILY_HARMONIC_VEC, 3, k=[4.0, -1.0, 2.5], a=1.0, b=2.0,
+                                 n_samples=100_000, index=8), 42, 1, 0)]
+    for f, seed, trial, cb in cases:
+        st = mcb.TrialStats()
+        rc = ref.ref_direct_mc(mcb.to_dsl(f).encode(), ctypes.byref(f), seed, trial, cb, ctypes.byref(st))
+        assert rc == 0, ref.ref_last_error()
+        dm.append({"desc": desc_json(f), "seed": seed, "trial": trial, "chunk_base": cb,
+                   "estimate": stats_json(st)})
+    g["direct_mc"] = dm
+
+    # 4. run_batch: C1 and C3 shapes at reduced sample counts
+    rb = []
+    for name, (fns, seed, trials) in [("c1_1e5", workloads.c1(100_000)),
+                                      ("c3_1e5", workloads.c3(100_000)),
+                                      ("c2_first40_2e4", (workloads.c2(20_000)[0][:40], 20200814, 10))]:
+        out, mean, sd, ok, _ = _oracle.ref_run_batch(fns, seed, trials, workers=0)
+        rb.append({"name": name, "seed": seed, "trials": trials,
+                   "descs": [desc_json(f) for f in fns],
+                   "per_trial": [[stats_json(_as_stats(out[i, t])) for t in range(trials)]
+                                 for i in range(len(fns))],
+                   "mean": [H(x) for x in mean], "trial_stddev": [H(x) for x in sd],
+                   "ok": [int(x) for x in ok]})
+    g["run_batch"] = rb
+
+    # 5. reference known answers (tests/test_job_io.cpp:140-171)
+    ks = np.zeros(100)
+    seed = ctypes.c_uint64()
+    trials = ctypes.c_uint32()
+    assert ref.ref_harmonic_job(100, 1_000_000, ks.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                ctypes.byref(seed), ctypes.byref(trials)) == 0
+    g["harmonic_job"] = {"k": [H(k) for k in ks], "seed": seed.value, "trials": trials.value,
+                         "analytic": [H(ref.ref_analytic_harmonic(n)) for n in range(1, 101)]}
+
+    with open(os.path.join(HERE, "golden.json"), "w") as fh:
+        json.dump(g, fh, indent=1)
+    print("wrote", os.path.join(HERE, "golden.json"))
+
+
+def _as_stats(row):
+    st = mcb.TrialStats()
+    st.value, st.std_error = float(row["value"]), float(row["std_error"])
+    st.n_samples, st.n_nonfinite = int(row["n_samples"]), int(row["n_nonfinite"])
+    st.status, st.nonfinite_warning = int(row["status"]), int(row["nonfinite_warning"])
+    return st
+
+
+if __name__ == "__main__":
+    main()

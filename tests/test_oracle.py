@@ -1,0 +1,176 @@
+"""Pin the CPU oracle (oracle/mcb_oracle.c) before trusting it.
+
+It must reproduce, BIT-EXACTLY, (1) the Random123 Philox4x32-10 known-answer
+vectors, (2) the survey's golden vectors, (3) every
+golden vector the reference itself produced (tests/golden/golden.json, made by
+tests/golden/make_golden.py from the reference compiled from its sources),
+and (4) the reference tests' known answers (tests/test_job_io.cpp:140-171,
+tests/test_estimator.cpp:44-62)."""
+import ctypes
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from tests import _oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.json")
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(GOLDEN) as fh:
+        return json.load(fh)
+
+
+def fx(h):
+    return float.fromhex(h)
+
+
+def desc_from(d):
+    import paper_2104_10073_b200 as mcb
+    f = mcb.Integrand()
+    f.family, f.dim, f.integrand_index, f.flags = d["family"], d["dim"], d["integrand_index"], d["flags"]
+    f.n_samples = d["n_samples"]
+    f.a, f.b = fx(d["a"]), fx(d["b"])
+    for j in range(8):
+        f.k[j], f.low[j], f.high[j] = fx(d["k"][j]), fx(d["low"][j]), fx(d["high"][j])
+    return f
+
+
+def test_philox_random123_kats():
+    # Random123 kat_vectors for philox4x32_10 (also SURVEY.md §8(c))
+    assert _oracle.philox([0, 0, 0, 0], [0, 0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert _oracle.philox([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2) == [0x408F276D, 0x41C83B0E,
+                                                                  0xA20BC7C6, 0x6D5451FD]
+    assert _oracle.philox([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+                          [0xA4093822, 0x299F31D0]) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420,
+                                                        0x24126EA1]
+
+
+def test_survey_appendix_a_vectors(oracle):
+    assert _oracle.stream_key(20200814, 0) == (0x37BA30CA, 0xCCC782D2)
+    assert _oracle.philox([0, 0, 0, 0], [0x37BA30CA, 0xCCC782D2]) == [0xC9901A70, 0xEE6ECC27,
+                                                                      0x4FC12354, 0x6FEDE878]
+    p = _oracle.sample_uniform([0.0], [1.0], 0, 0, 0, 0, 0, 4).ravel()
+    assert [v.hex() for v in p] == [float.fromhex("0x1.a9e3e15891c3dp-1").hex(),
+                                    (0.3229675943419219).hex(), (0.99678950396949695).hex(),
+                                    (0.84404300165309387).hex()]
+    pts = _oracle.sample_uniform([0.0] * 4, [1.0] * 4, 20200814, 0, 0, 0, 0, 2)
+    assert list(pts[0]) == [0.78735509163964956, 0.31154080211120283, 0.054781718112023703,
+                            0.33030979303343322]
+    assert list(pts[1]) == [0.75605201863373872, 0.5490284010596278, 0.49091535111693241,
+                            0.36042167796002622]
+    p99 = _oracle.sample_uniform([0.0] * 4, [1.0] * 4, 20200814, 99, 9, 15, 0, 1)
+    assert list(p99[0]) == [0.43711045983064589, 0.90531582227844243, 0.8328836986772683,
+                            0.88764996157409182]
+    p3 = _oracle.sample_uniform([0.0] * 3, [1.0] * 3, 7, 1, 0, 0, 0, 3)
+    assert list(p3[2]) == [0.45311502163963258, 0.07281954660657286, 0.36230039382735879]
+
+
+def test_points_match_reference_golden(golden):
+    for case in golden["points"]:
+        lo = [fx(x) for x in case["low"]]
+        hi = [fx(x) for x in case["high"]]
+        want = np.array([[fx(x) for x in row] for row in case["points"]])
+        got = _oracle.sample_uniform(lo, hi, case["seed"], case["integrand"], case["trial"],
+                                     case["chunk"], 0, len(want))
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), case
+        # first_point offset (used by the GPU point dumps) must give the same stream
+        tail = _oracle.sample_uniform(lo, hi, case["seed"], case["integrand"], case["trial"],
+                                      case["chunk"], 3, len(want) - 3)
+        assert np.array_equal(tail.view(np.uint64), want[3:].view(np.uint64))
+
+
+def test_family_values_match_reference_golden(golden):
+    for case in golden["evals"]:
+        f = desc_from(case["desc"])
+        pts = _oracle.sample_uniform([f.low[j] for j in range(f.dim)],
+                                     [f.high[j] for j in range(f.dim)], case["seed"],
+                                     f.integrand_index, case["trial"], case["chunk"], 0,
+                                     len(case["values"]))
+        got = _oracle.eval_points(f, pts)
+        want = np.array([fx(v) for v in case["values"]])
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), case["desc"]["source"]
+
+
+def test_direct_mc_matches_reference_golden(golden):
+    for case in golden["direct_mc"]:
+        f = desc_from(case["desc"])
+        st = _oracle.direct_mc(f, case["seed"], case["trial"], case["chunk_base"])
+        e = case["estimate"]
+        assert st.value == fx(e["value"]) and st.std_error == fx(e["std_error"]), case["desc"]["source"]
+        assert (st.n_samples, st.n_nonfinite, st.status) == (e["n_samples"], e["n_nonfinite"], e["status"])
+
+
+def test_run_batch_matches_reference_golden(golden, oracle):
+    for rb in golden["run_batch"]:
+        fns = [desc_from(d) for d in rb["descs"]]
+        out = _oracle.run_direct(fns, rb["seed"], rb["trials"], n_threads=4)
+        for i in range(len(fns)):
+            for t in range(rb["trials"]):
+                e = rb["per_trial"][i][t]
+                assert out[i, t]["value"] == fx(e["value"])
+                assert out[i, t]["std_error"] == fx(e["std_error"])
+            per = out[i]
+            mean, sd, nok = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint32()
+            from paper_2104_10073_b200 import TrialStats
+            oracle.orc_summarize_trials(per.ctypes.data_as(ctypes.POINTER(TrialStats)), rb["trials"],
+                                        ctypes.byref(mean), ctypes.byref(sd), ctypes.byref(nok))
+            assert mean.value == fx(rb["mean"][i]) and sd.value == fx(rb["trial_stddev"][i])
+
+
+def test_worker_count_invariance(oracle):
+    from paper_2104_10073_b200 import workloads
+    fns, seed, trials = workloads.c1(20_000)
+    a = _oracle.run_direct(fns[:10], seed, 3, n_threads=1)
+    b = _oracle.run_direct(fns[:10], seed, 3, n_threads=4)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_reference_known_answers(golden, oracle):
+    # tests/test_job_io.cpp:140-171 and tests/test_estimator.cpp:54-62
+    k = [fx(x) for x in golden["harmonic_job"]["k"]]
+    assert k[0] == pytest.approx(8.116902097686662, rel=1e-15)
+    assert k[99] == pytest.approx(23.873241463784303, rel=1e-15)
+    assert [oracle.orc_harmonic_k(n) for n in range(1, 101)] == k
+    an = [fx(x) for x in golden["harmonic_job"]["analytic"]]
+    assert an[0] == pytest.approx(-0.001999358381010922, rel=1e-12)
+    assert an[49] == pytest.approx(0.00032173407630372935, rel=1e-12)
+    assert an[99] == pytest.approx(-8.269899026451183e-06, rel=1e-9)
+    for n in (1, 50, 100):
+        assert oracle.orc_harmonic_closed_form(k[n - 1], 4) == pytest.approx(an[n - 1], rel=1e-12)
+    assert golden["harmonic_job"]["seed"] == 20200814 and golden["harmonic_job"]["trials"] == 10
+
+
+def test_constant_integrand_exact(oracle):
+    import paper_2104_10073_b200 as mcb
+    # tests/test_estimator.cpp:44-52: 7 on [0,2]^2 -> 28 exactly, std_error 0
+    f = mcb.harmonic(0.0, 2, a=7.0, b=3.0, low=[0, 0], high=[2, 2], n_samples=1000)
+    st = _oracle.direct_mc(f, 1)
+    assert st.value == 28.0 and st.std_error == 0.0 and st.n_samples == 1000
+
+
+def test_oracle_against_live_reference_random_cases(oracle):
+    """When oracle/_ref is built (build container), cross-check random cases live."""
+    ref = _oracle.load_ref()
+    if ref is None:
+        pytest.skip("oracle/_ref not built here (GPU box / fresh checkout)")
+    import paper_2104_10073_b200 as mcb
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        fam = int(rng.integers(0, 4))
+        dim = int(rng.integers(3, 8))
+        lo = rng.uniform(-1, 0.5, dim)
+        hi = lo + rng.uniform(0.1, 2, dim)
+        f = mcb.make_integrand(fam, dim, k=list(rng.uniform(-9, 9, 8)), a=float(rng.uniform(-2, 2)),
+                               b=float(rng.uniform(-2, 2)), low=lo, high=hi,
+                               n_samples=int(rng.integers(2, 140_000)), index=int(rng.integers(0, 999)))
+        seed = int(rng.integers(0, 2**63))
+        st_o = _oracle.direct_mc(f, seed, trial=trial, chunk_base=trial)
+        st_r = mcb.TrialStats()
+        assert ref.ref_direct_mc(mcb.to_dsl(f).encode(), ctypes.byref(f), seed, trial, trial,
+                                 ctypes.byref(st_r)) == 0
+        assert (st_o.value, st_o.std_error) == (st_r.value, st_r.std_error), mcb.to_dsl(f)
