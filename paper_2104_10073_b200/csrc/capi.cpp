@@ -290,20 +290,6 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
 
 // ---- plans -------------------------------------------------------------------
 
-struct mcb_plan {
-  int device = 0;
-  uint64_t n_fns = 0;
-  uint32_t trials = 0;
-  uint64_t n_tiles = 0;
-  uint64_t total_samples = 0;
-  uint64_t philox_blocks = 0;
-  std::vector<GroupLaunch> groups;
-  FnDesc* d_fns = nullptr;
-  uint32_t* d_tile_fn = nullptr;
-  TilePartial* d_part = nullptr;
-  mcb_trial_stats* d_out = nullptr;
-};
-
 namespace {
 
 struct DeviceGuard {
@@ -317,18 +303,35 @@ struct DeviceGuard {
   }
 };
 
+// Device checks are cached: cudaGetDeviceProperties is slow and this runs
+// on every call.
 mcb_status check_device(int device) {
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+  static std::mutex mu;
+  static int count = -1;
+  static std::map<int, int> major;
+  std::lock_guard<std::mutex> lock(mu);
+  if (count < 0) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    count = n;
+  }
+  if (count == 0)
     return fail(MCB_ERR_NO_DEVICE, "no CUDA device visible (the mcb path has no CPU fallback)");
-  if (device < 0 || device >= n)
+  if (device < 0 || device >= count)
     return fail(MCB_ERR_INVALID_ARGUMENT, "device ordinal " + std::to_string(device) +
-                                              " out of range (" + std::to_string(n) + " visible)");
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
-    return fail(MCB_ERR_NO_DEVICE, "cannot query device");
-  if (prop.major != 10)
-    return fail(MCB_ERR_NO_DEVICE, std::string("device ") + prop.name +
+                                              " out of range (" + std::to_string(count) + " visible)");
+  auto it = major.find(device);
+  if (it == major.end()) {
+    int m = 0;
+    if (cudaDeviceGetAttribute(&m, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess)
+      return fail(MCB_ERR_NO_DEVICE, "cannot query device");
+    it = major.emplace(device, m).first;
+  }
+  if (it->second != 10)
+    return fail(MCB_ERR_NO_DEVICE, "device " + std::to_string(device) +
                                        " is not sm_100 (this build targets sm_100a only)");
   return MCB_OK;
 }
@@ -348,6 +351,192 @@ mcb_status validate_for_run(const mcb_integrand* fns, size_t n_fns, uint32_t tri
   return fail(MCB_ERR_VALIDATION, msg);
 }
 
+// Philox blocks one sample pair really needs (blocks holding only draws of
+// coordinates a family never reads are skipped by eval_pair).
+uint64_t blocks_per_pair(uint32_t family, uint32_t dim) {
+  const uint32_t used = family == MCB_FAMILY_ABS2 ? 2u : (family == MCB_FAMILY_ABS3 ? 3u : dim);
+  uint64_t n = 0;
+  for (uint32_t i = 0; i < dim; ++i)
+    if ((2 * i) % dim < used || (2 * i + 1) % dim < used) ++n;
+  return n;
+}
+
+// Host half of a plan: device descriptors grouped by (family, dim, variant)
+// with tile bases assigned; no CUDA calls.
+struct HostPlan {
+  std::vector<FnDesc> descs;  // group order
+  std::vector<GroupLaunch> groups;
+  uint64_t n_tiles = 0, total_samples = 0, philox_blocks = 0;
+};
+
+mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
+                           uint32_t chunk_base, uint32_t trial_base, HostPlan& hp) {
+  std::vector<Prepared> prep(n_fns);
+  for (size_t i = 0; i < n_fns; ++i) prep[i] = prepare(fns[i], seed, chunk_base, trial_base);
+  std::vector<size_t> order(n_fns);
+  std::iota(order.begin(), order.end(), size_t(0));
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+    auto kx = std::make_tuple(fns[x].family, fns[x].dim, prep[x].variant);
+    auto ky = std::make_tuple(fns[y].family, fns[y].dim, prep[y].variant);
+    return kx < ky;
+  });
+  hp.descs.resize(n_fns);
+  uint64_t tile = 0;
+  for (size_t r = 0; r < n_fns; ++r) {
+    const size_t i = order[r];
+    FnDesc d = prep[i].d;
+    d.tile_base = tile;
+    d.out_slot = i;
+    const uint64_t nt = uint64_t(d.n_chunks) * trials;
+    const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
+    if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
+        hp.groups.back().variant != var)
+      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0});
+    hp.groups.back().n_tiles += nt;
+    tile += nt;
+    hp.descs[r] = d;
+    hp.total_samples += fns[i].n_samples * trials;
+    const uint64_t full = fns[i].n_samples / MCB_CHUNK_SIZE, last = fns[i].n_samples % MCB_CHUNK_SIZE;
+    const uint64_t pairs = full * (MCB_CHUNK_SIZE / 2) + (last + 1) / 2;
+    hp.philox_blocks += pairs * blocks_per_pair(fns[i].family, fns[i].dim) * trials;
+  }
+  for (const auto& g : hp.groups)
+    if (!mcb::detail::variant_supported(g.family, g.dim, g.variant))
+      return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
+  hp.n_tiles = tile;
+  return MCB_OK;
+}
+
+// Growable device buffers of a plan.
+struct DevBuf {
+  FnDesc* fns = nullptr;
+  uint32_t* tile_fn = nullptr;
+  TilePartial* part = nullptr;
+  mcb_trial_stats* out = nullptr;
+  size_t cap_fns = 0, cap_tiles = 0, cap_part = 0, cap_out = 0;
+
+  template <class T>
+  static cudaError_t grow(T*& p, size_t& cap, size_t need) {
+    if (need <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t n = std::max<size_t>(need, 1);
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * n);
+    if (e == cudaSuccess) cap = n;
+    return e;
+  }
+  cudaError_t reserve(size_t n_fns, size_t n_tiles, size_t n_out) {
+    cudaError_t e;
+    if ((e = grow(fns, cap_fns, n_fns)) != cudaSuccess) return e;
+    if ((e = grow(tile_fn, cap_tiles, n_tiles)) != cudaSuccess) return e;
+    if ((e = grow(part, cap_part, n_tiles)) != cudaSuccess) return e;
+    return grow(out, cap_out, n_out);
+  }
+  void release() {
+    if (fns) cudaFree(fns);
+    if (tile_fn) cudaFree(tile_fn);
+    if (part) cudaFree(part);
+    if (out) cudaFree(out);
+    *this = DevBuf{};
+  }
+};
+
+// Enqueue: descriptor upload (from `staged`, pinned or not) + tile table +
+// fused kernels + ordered combine, all on `s`.
+mcb_status enqueue_run(const HostPlan& hp, DevBuf& buf, uint32_t trials, const FnDesc* staged,
+                       bool upload, cudaStream_t s) {
+  cudaError_t e;
+  const uint32_t n_fns = uint32_t(hp.descs.size());
+  if (upload) {
+    if ((e = cudaMemcpyAsync(buf.fns, staged, sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync(descriptors)");
+    if ((e = mcb::detail::launch_expand_tiles(buf.fns, n_fns, trials, buf.tile_fn, s)) != cudaSuccess)
+      return cuda_fail(e, "launch k_expand_tiles");
+  }
+  for (const auto& g : hp.groups)
+    if ((e = mcb::detail::launch_direct_group(g, buf.fns, buf.tile_fn, buf.part, s)) != cudaSuccess)
+      return cuda_fail(e, "launch k_direct");
+  if ((e = mcb::detail::launch_combine(buf.fns, n_fns, trials, buf.part, buf.out, s)) != cudaSuccess)
+    return cuda_fail(e, "launch k_combine");
+  return MCB_OK;
+}
+
+// Per-device context reused by mcb_run_direct: stream, device buffers and
+// pinned staging, so a call costs H2D + kernels + D2H, not allocations.
+struct DeviceCtx {
+  std::mutex mu;
+  bool ready = false;
+  cudaStream_t stream = nullptr;
+  DevBuf buf;
+  FnDesc* h_descs = nullptr;
+  size_t h_descs_cap = 0;
+  mcb_trial_stats* h_out = nullptr;
+  size_t h_out_cap = 0;
+};
+
+DeviceCtx& device_ctx(int device) {
+  static std::mutex mu;
+  static std::map<int, DeviceCtx*> ctxs;  // never freed: lives for the process
+  std::lock_guard<std::mutex> lock(mu);
+  DeviceCtx*& c = ctxs[device];
+  if (!c) c = new DeviceCtx();
+  return *c;
+}
+
+template <class T>
+cudaError_t grow_pinned(T*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return cudaSuccess;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  cap = 0;
+  const size_t n = std::max<size_t>(need, 1);
+  cudaError_t e = cudaMallocHost(&p, sizeof(T) * n);
+  if (e == cudaSuccess) cap = n;
+  return e;
+}
+
+// One shard of mcb_run_direct on one device (synchronous).
+mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
+                     int device, mcb_trial_stats* out) {
+  HostPlan hp;
+  mcb_status st = build_host_plan(fns, n_fns, seed, trials, 0, 0, hp);
+  if (st != MCB_OK) return st;
+  DeviceCtx& c = device_ctx(device);
+  std::lock_guard<std::mutex> lock(c.mu);
+  DeviceGuard guard(device);
+  cudaError_t e;
+  if (!c.ready) {
+    if ((e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+    c.ready = true;
+  }
+  const size_t n_out = n_fns * trials;
+  if ((e = c.buf.reserve(n_fns, hp.n_tiles, n_out)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  if ((e = grow_pinned(c.h_descs, c.h_descs_cap, n_fns)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  if ((e = grow_pinned(c.h_out, c.h_out_cap, n_out)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  std::memcpy(c.h_descs, hp.descs.data(), sizeof(FnDesc) * n_fns);
+  if ((st = enqueue_run(hp, c.buf, trials, c.h_descs, true, c.stream)) != MCB_OK) return st;
+  if ((e = cudaMemcpyAsync(c.h_out, c.buf.out, sizeof(mcb_trial_stats) * n_out, cudaMemcpyDeviceToHost,
+                           c.stream)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync(results)");
+  if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  std::memcpy(out, c.h_out, sizeof(mcb_trial_stats) * n_out);
+  return MCB_OK;
+}
+
+}  // namespace
+
+struct mcb_plan {
+  int device = 0;
+  uint64_t n_fns = 0;
+  uint32_t trials = 0;
+  HostPlan hp;
+  DevBuf buf;
+};
+
+namespace {
+
 mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
                             uint32_t trials, int device, uint32_t chunk_base,
                             uint32_t trial_base, mcb_plan** out) {
@@ -359,92 +548,37 @@ mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t see
         return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
   }
   if ((st = check_device(device)) != MCB_OK) return st;
-
-  std::vector<Prepared> prep(n_fns);
-  for (size_t i = 0; i < n_fns; ++i) prep[i] = prepare(fns[i], seed, chunk_base, trial_base);
-  // groups: (family, dim, variant), stable in job order
-  std::vector<size_t> order(n_fns);
-  std::iota(order.begin(), order.end(), size_t(0));
-  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
-    auto kx = std::make_tuple(fns[x].family, fns[x].dim, prep[x].variant);
-    auto ky = std::make_tuple(fns[y].family, fns[y].dim, prep[y].variant);
-    return kx < ky;
-  });
   auto plan = new mcb_plan();
   plan->device = device;
   plan->n_fns = n_fns;
   plan->trials = trials;
-  std::vector<FnDesc> host(n_fns);
-  uint64_t tile = 0;
-  for (size_t r = 0; r < n_fns; ++r) {
-    const size_t i = order[r];
-    FnDesc d = prep[i].d;
-    d.tile_base = tile;
-    d.out_slot = i;
-    const uint64_t nt = uint64_t(d.n_chunks) * trials;
-    const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
-    if (plan->groups.empty() || plan->groups.back().family != fam ||
-        plan->groups.back().dim != dim || plan->groups.back().variant != var)
-      plan->groups.push_back(GroupLaunch{fam, dim, var, tile, 0});
-    plan->groups.back().n_tiles += nt;
-    tile += nt;
-    host[r] = d;
-    plan->total_samples += fns[i].n_samples * trials;
-    // Philox blocks per chunk: pairs * dim (blocks of unused ABS coordinates skipped)
-    const uint64_t used_dim = fam == MCB_FAMILY_ABS2   ? std::min<uint32_t>(dim, 2)
-                              : fam == MCB_FAMILY_ABS3 ? std::min<uint32_t>(dim, 3)
-                                                       : uint64_t(dim);
-    (void)used_dim;
-    const uint64_t full = fns[i].n_samples / MCB_CHUNK_SIZE, last = fns[i].n_samples % MCB_CHUNK_SIZE;
-    const uint64_t blocks_per_fn_trial =
-        full * (MCB_CHUNK_SIZE / 2) * uint64_t(dim) + ((last + 1) / 2) * uint64_t(dim);
-    plan->philox_blocks += blocks_per_fn_trial * trials;
+  if ((st = build_host_plan(fns, n_fns, seed, trials, chunk_base, trial_base, plan->hp)) != MCB_OK) {
+    delete plan;
+    return st;
   }
-  for (const auto& g : plan->groups)
-    if (!mcb::detail::variant_supported(g.family, g.dim, g.variant)) {
-      delete plan;
-      return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
-    }
-  plan->n_tiles = tile;
-
   DeviceGuard guard(device);
-  auto cleanup = [&](cudaError_t e, const char* what) {
+  cudaError_t e = plan->buf.reserve(n_fns, plan->hp.n_tiles, n_fns * trials);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(plan->buf.fns, plan->hp.descs.data(), sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = mcb::detail::launch_expand_tiles(plan->buf.fns, uint32_t(n_fns), trials, plan->buf.tile_fn, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
     mcb_plan_destroy(plan);
-    return cuda_fail(e, what);
-  };
-  cudaError_t e;
-  if ((e = cudaMalloc(&plan->d_fns, sizeof(FnDesc) * std::max<size_t>(n_fns, 1))) != cudaSuccess)
-    return cleanup(e, "cudaMalloc(fns)");
-  if ((e = cudaMalloc(&plan->d_tile_fn, sizeof(uint32_t) * std::max<uint64_t>(tile, 1))) != cudaSuccess)
-    return cleanup(e, "cudaMalloc(tile_fn)");
-  if ((e = cudaMalloc(&plan->d_part, sizeof(TilePartial) * std::max<uint64_t>(tile, 1))) != cudaSuccess)
-    return cleanup(e, "cudaMalloc(partials)");
-  if ((e = cudaMalloc(&plan->d_out, sizeof(mcb_trial_stats) * std::max<uint64_t>(n_fns * trials, 1))) != cudaSuccess)
-    return cleanup(e, "cudaMalloc(out)");
-  if ((e = cudaMemcpy(plan->d_fns, host.data(), sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice)) != cudaSuccess)
-    return cleanup(e, "cudaMemcpy(fns)");
-  if ((e = mcb::detail::launch_expand_tiles(plan->d_fns, uint32_t(n_fns), trials, plan->d_tile_fn, 0)) != cudaSuccess)
-    return cleanup(e, "expand_tiles");
-  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(e, "cudaDeviceSynchronize");
+    return cuda_fail(e, "plan setup");
+  }
   *out = plan;
   return MCB_OK;
 }
 
 mcb_status plan_launch_impl(mcb_plan* plan, cudaStream_t s) {
   DeviceGuard guard(plan->device);
-  for (const auto& g : plan->groups) {
-    cudaError_t e = mcb::detail::launch_direct_group(g, plan->d_fns, plan->d_tile_fn, plan->d_part, s);
-    if (e != cudaSuccess) return cuda_fail(e, "launch k_direct");
-  }
-  cudaError_t e = mcb::detail::launch_combine(plan->d_fns, uint32_t(plan->n_fns), plan->trials,
-                                              plan->d_part, plan->d_out, s);
-  if (e != cudaSuccess) return cuda_fail(e, "launch k_combine");
-  return MCB_OK;
+  return enqueue_run(plan->hp, plan->buf, plan->trials, nullptr, false, s);
 }
 
 mcb_status plan_download_impl(mcb_plan* plan, mcb_trial_stats* out, cudaStream_t s) {
   DeviceGuard guard(plan->device);
-  MCB_CUDA(cudaMemcpyAsync(out, plan->d_out, sizeof(mcb_trial_stats) * plan->n_fns * plan->trials,
+  MCB_CUDA(cudaMemcpyAsync(out, plan->buf.out, sizeof(mcb_trial_stats) * plan->n_fns * plan->trials,
                            cudaMemcpyDeviceToHost, s));
   MCB_CUDA(cudaStreamSynchronize(s));
   return MCB_OK;
@@ -592,12 +726,12 @@ mcb_status mcb_plan_get_info(const mcb_plan* plan, mcb_plan_info* info) {
   std::memset(info, 0, sizeof *info);
   info->n_fns = plan->n_fns;
   info->trials = plan->trials;
-  info->n_groups = uint32_t(plan->groups.size());
-  info->n_tiles = plan->n_tiles;
-  info->total_samples = plan->total_samples;
-  info->philox_blocks = plan->philox_blocks;
+  info->n_groups = uint32_t(plan->hp.groups.size());
+  info->n_tiles = plan->hp.n_tiles;
+  info->total_samples = plan->hp.total_samples;
+  info->philox_blocks = plan->hp.philox_blocks;
   uint32_t launches = 1;  // k_combine
-  for (const auto& g : plan->groups) launches += uint32_t((g.n_tiles + 0x7FFFFFFEull) / 0x7FFFFFFFull);
+  for (const auto& g : plan->hp.groups) launches += uint32_t((g.n_tiles + 0x7FFFFFFEull) / 0x7FFFFFFFull);
   info->launches_per_run = launches;
   return MCB_OK;
 }
@@ -606,10 +740,7 @@ void mcb_plan_destroy(mcb_plan* plan) {
   if (!plan) return;
   {
     DeviceGuard guard(plan->device);
-    if (plan->d_fns) cudaFree(plan->d_fns);
-    if (plan->d_tile_fn) cudaFree(plan->d_tile_fn);
-    if (plan->d_part) cudaFree(plan->d_part);
-    if (plan->d_out) cudaFree(plan->d_out);
+    plan->buf.release();
   }
   delete plan;
 }
@@ -638,22 +769,8 @@ mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
     if (mine.empty()) return;
     std::vector<mcb_integrand> sub(mine.size());
     for (size_t r = 0; r < mine.size(); ++r) sub[r] = fns[mine[r]];
-    mcb_plan* plan = nullptr;
-    mcb_status s = plan_create_impl(sub.data(), sub.size(), seed, trials, devs[w], 0, 0, &plan);
     std::vector<mcb_trial_stats> res(sub.size() * trials);
-    cudaStream_t stream = nullptr;
-    if (s == MCB_OK) {
-      DeviceGuard guard(devs[w]);
-      if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess)
-        s = fail(MCB_ERR_CUDA, "cudaStreamCreate failed");
-    }
-    if (s == MCB_OK) s = plan_launch_impl(plan, stream);
-    if (s == MCB_OK) s = plan_download_impl(plan, res.data(), stream);
-    if (stream) {
-      DeviceGuard guard(devs[w]);
-      cudaStreamDestroy(stream);
-    }
-    mcb_plan_destroy(plan);
+    const mcb_status s = run_shard(sub.data(), sub.size(), seed, trials, devs[w], res.data());
     status[w] = s;
     if (s != MCB_OK) {
       errors[w] = g_last_error;
@@ -793,7 +910,7 @@ mcb_status mcb_probe_mul_peak(int device, double ms, double* muls_per_s) {
   cudaEventDestroy(b);
   cudaFree(sink);
   if (e != cudaSuccess) return cuda_fail(e, "mul_probe");
-  *muls_per_s = double(ctas) * 256.0 * 8.0 * double(iters) / (double(elapsed) * 1e-3);
+  *muls_per_s = double(ctas) * 256.0 * 16.0 * double(iters) / (double(elapsed) * 1e-3);
   return MCB_OK;
 }
 

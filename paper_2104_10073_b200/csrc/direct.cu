@@ -65,9 +65,21 @@ __global__ void __launch_bounds__(kThreads) k_direct(const FnDesc* __restrict__ 
 
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
-  for (uint32_t q = threadIdx.x; q < pairs; q += kThreads) {
-    double f0, f1;
-    dev::eval_pair<FAM, D, UNIT_DOM, UNIT_COEF, CHECK>(f, c_sincos, tab, P, q, f0, f1);
+  // Software pipeline: iteration i folds pair q_i's transcendental part
+  // (FP64-heavy) while generating pair q_{i+1} (integer-heavy), so the two
+  // independent streams interleave in one instruction window.  The last
+  // iteration generates one pair past the chunk; it is discarded.
+  const uint32_t iters = threadIdx.x < pairs ? (pairs - threadIdx.x + kThreads - 1) / kThreads : 0u;
+  double a0, a1;
+  dev::gen_pair<FAM, D, UNIT_DOM, CHECK>(f, P, threadIdx.x, a0, a1);
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint32_t q = threadIdx.x + it * kThreads;
+    double b0, b1;
+    dev::gen_pair<FAM, D, UNIT_DOM, CHECK>(f, P, q + kThreads, b0, b1);
+    const double f0 = dev::finish<FAM, UNIT_COEF, CHECK>(f, c_sincos, tab, a0);
+    const double f1 = dev::finish<FAM, UNIT_COEF, CHECK>(f, c_sincos, tab, a1);
+    a0 = b0;
+    a1 = b1;
     const bool has1 = 2 * q + 1 < count;
     double g0 = __dsub_rn(f0, f.shift);
     double g1 = __dsub_rn(f1, f.shift);
@@ -212,16 +224,17 @@ __global__ void k_debug_eval(const FnDesc* __restrict__ fn, uint32_t trial, uint
   out[2 * uint64_t(i) + 1] = f1;
 }
 
-// Integer-multiply pipe probe: 8 independent 32x32->64 multiply chains per
-// thread (same mulhilo as Philox).  Result folded into `sink` so nothing is
-// dead code.
+// Integer-multiply pipe probe: 16 independent 32x32->64 multiply chains per
+// thread (the same mulhilo as Philox, i.e. IMAD.WIDE.U32 by a constant),
+// folded with one LOP3 each like a Philox round.  The result feeds `sink`
+// so nothing is dead code.
 __global__ void __launch_bounds__(256) k_mul_probe(uint32_t* sink, int iters) {
-  uint32_t x[8];
+  uint32_t x[16];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 2654435761u + i * 40503u + blockIdx.x;
+  for (int i = 0; i < 16; ++i) x[i] = threadIdx.x * 2654435761u + i * 40503u + blockIdx.x;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 16; ++i) {
       uint32_t hi, lo;
       dev::mulhilo(i & 1 ? dev::kM1 : dev::kM0, x[i], hi, lo);
       x[i] = hi ^ lo;
@@ -229,7 +242,7 @@ __global__ void __launch_bounds__(256) k_mul_probe(uint32_t* sink, int iters) {
   }
   uint32_t acc = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc ^= x[i];
+  for (int i = 0; i < 16; ++i) acc ^= x[i];
   if (acc == 0x12345678u) sink[blockIdx.x] = acc;
 }
 

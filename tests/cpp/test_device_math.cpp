@@ -1,0 +1,124 @@
+// Host build of the device arithmetic (paper_2104_10073_b200/csrc/mcb_device.cuh,
+// compiled with g++ -ffp-contract=off) checked against the C oracle
+// (oracle/mcb_oracle.c, itself pinned to the reference).  Runs without a GPU.
+//
+//  1. philox_block(make_prefix(...)) == philox_block of the reference
+//     (src/sampling.cpp:51-70) for random keys / counters, incl. chunk, trial > 0
+//  2. u_scaled(hi, lo) * 2^-64 == to_unit_double(hi, lo) bit-exactly
+//     (src/sampling.cpp:72-75)
+//  3. the 2^-64 folding used by the FAST variants is bit-exact
+//  4. sincos_fast is within 2 ulp of the correctly rounded sin/cos
+//  5. the quadrant-coefficient form of a*cos + b*sin is bit-identical to the
+//     literal expression evaluated with the same sin/cos values
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "mcb_device.cuh"
+
+extern "C" {
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+double orc_to_unit_double(uint32_t hi, uint32_t lo);
+}
+
+using namespace mcb::dev;
+
+static int g_fail = 0;
+#define CHECK(cond, ...)                      \
+  do {                                        \
+    if (!(cond)) {                            \
+      if (g_fail < 20) {                      \
+        std::printf("FAIL %s:%d ", __FILE__, __LINE__); \
+        std::printf(__VA_ARGS__);             \
+        std::printf("\n");                    \
+      }                                       \
+      ++g_fail;                               \
+    }                                         \
+  } while (0)
+
+static uint64_t bits(double x) {
+  uint64_t b;
+  std::memcpy(&b, &x, 8);
+  return b;
+}
+
+static double ulp_err(double got, long double exact) {
+  const double e = double(exact);
+  const double ulp = std::nextafter(std::fabs(e), INFINITY) - std::fabs(e);
+  return double(std::fabs((long double)got - exact)) / ulp;
+}
+
+int main() {
+  std::mt19937_64 rng(20200814);
+  // 1. Philox with the CTA prefix
+  for (int i = 0; i < 200000; ++i) {
+    const uint32_t k0 = uint32_t(rng()), k1 = uint32_t(rng());
+    const uint32_t chunk = (i & 3) ? uint32_t(rng()) : 0u, trial = (i & 1) ? uint32_t(rng()) : 0u;
+    const uint32_t b = uint32_t(rng() % 300000);
+    PhiloxPrefix P = make_prefix(k0, k1, chunk, trial);
+    uint32_t got[4], want[4];
+    philox_block(P, b, got);
+    const uint32_t ctr[4] = {b, 0u, chunk, trial}, key[2] = {k0, k1};
+    orc_philox4x32_10(ctr, key, want);
+    CHECK(std::memcmp(got, want, 16) == 0, "philox k=%08x,%08x b=%u", k0, k1, b);
+  }
+  // 2. exact 53-bit conversion
+  const uint32_t edge[] = {0u, 1u, 0x7FFu, 0x800u, 0x7FFFFFFFu, 0x80000000u, 0xFFFFF7FFu, 0xFFFFFFFFu};
+  for (uint32_t hi : edge)
+    for (uint32_t lo : edge)
+      CHECK(bits(u_scaled(hi, lo) * kTwoM64) == bits(orc_to_unit_double(hi, lo)), "u53 %08x %08x", hi, lo);
+  for (int i = 0; i < 1000000; ++i) {
+    const uint32_t hi = uint32_t(rng()), lo = uint32_t(rng());
+    CHECK(bits(u_scaled(hi, lo) * kTwoM64) == bits(orc_to_unit_double(hi, lo)), "u53 %08x %08x", hi, lo);
+  }
+  // 3. folding: RN(k' * ((v1+v2)+v3)) == RN(k * ((u1+u2)+u3)) with k' = k*2^-64,
+  //    and low + w'*v == low + w*u
+  for (int i = 0; i < 1000000; ++i) {
+    double v[3], u[3];
+    for (int j = 0; j < 3; ++j) {
+      v[j] = u_scaled(uint32_t(rng()), uint32_t(rng()));
+      u[j] = v[j] * kTwoM64;
+    }
+    const double k = std::ldexp(double(rng() >> 11) * 0x1p-53 + 0.5, int(rng() % 200) - 100);
+    const double sv = (v[0] + v[1]) + v[2], su = (u[0] + u[1]) + u[2];
+    CHECK(bits((k * kTwoM64) * sv) == bits(k * su), "fold k=%a", k);
+    const double w = std::ldexp(1.0 + double(rng() >> 12) * 0x1p-52, int(rng() % 60) - 30);
+    const double lo = double(int64_t(rng() % 2001) - 1000) * 0.37;
+    CHECK(bits(lo + (w * kTwoM64) * v[0]) == bits(lo + w * u[0]), "fold w=%a", w);
+  }
+  // 4. sincos_fast accuracy
+  const SinCosConsts K = MCB_SINCOS_CONSTS;
+  double max_s = 0, max_c = 0;
+  for (int e = -3; e <= 20; ++e) {
+    std::uniform_real_distribution<double> U(-std::ldexp(1.0, e), std::ldexp(1.0, e));
+    for (int i = 0; i < 200000; ++i) {
+      const double t = U(rng);
+      double s, c;
+      sincos_fast(K, t, s, c);
+      max_s = std::fmax(max_s, ulp_err(s, sinl((long double)t)));
+      max_c = std::fmax(max_c, ulp_err(c, cosl((long double)t)));
+    }
+  }
+  std::printf("sincos_fast max error: sin %.3f ulp, cos %.3f ulp\n", max_s, max_c);
+  CHECK(max_s < 2.0 && max_c < 2.0, "sincos accuracy sin %.3f cos %.3f", max_s, max_c);
+  // 5. quadrant-coefficient identity
+  for (int i = 0; i < 1000000; ++i) {
+    const double t = std::uniform_real_distribution<double>(-700, 700)(rng);
+    const double a = std::uniform_real_distribution<double>(-3, 3)(rng);
+    const double b = std::uniform_real_distribution<double>(-3, 3)(rng);
+    double sf, cf, s, c;
+    uint32_t q;
+    sincos_fast(K, t, sf, cf);
+    sincos_core(K, t, s, c, q);
+    const QuadCoef ab = quad_coef(a, b, int(q & 3u));
+    const double lit = (a * cf) + (b * sf);
+    const double quad = (ab.A * c) + (ab.B * s);
+    CHECK(bits(lit) == bits(quad), "quad a=%a b=%a t=%a", a, b, t);
+    const QuadCoef one = quad_coef(1.0, 1.0, int(q & 3u));
+    CHECK(bits(cf + sf) == bits(std::fma(one.A, c, one.B * s)), "unit quad t=%a", t);
+  }
+  std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -119,6 +119,8 @@ def test_family_values_vs_oracle(gpu):
             nan_g, nan_w = ~np.isfinite(got), ~np.isfinite(want)
             assert np.array_equal(nan_g, nan_w), gpu.to_dsl(f)
             g, w = got[~nan_w], want[~nan_w]
+            if len(w) == 0:
+                continue
             if f.family in (gpu.FAMILY_ABS2, gpu.FAMILY_ABS3):
                 assert np.array_equal(g, w), gpu.to_dsl(f)  # no transcendental: bit-exact
             else:
