@@ -21,7 +21,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmcb.so")
+LIB_PATH = os.environ.get("MCB_LIB") or os.path.join(_HERE, "libmcb.so")
 
 CHUNK_SIZE = 65536
 MAX_DIM = 8

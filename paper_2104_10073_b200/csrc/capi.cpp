@@ -206,7 +206,7 @@ struct Prepared {
 
 // Decide the kernel variant and fill the device descriptor.  FAST variants
 // need (host-proven, for every point of the domain): finite parameters,
-// |t| < 2^30 for the sincos reduction, no overflow of f, and exact 2^-64
+// |t| < 2^20 for the table reduction, no overflow of f, and exact 2^-64
 // folding.  Anything else runs the SAFE variant (libdevice sincos, counted
 // non-finite samples) — still on the GPU.
 Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
@@ -250,7 +250,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   if (fast && harm) {
     const double tmax = f.family == MCB_FAMILY_HARMONIC ? std::fabs(f.k[0]) * xmax * 1.0000001
                                                         : xmax * 1.0000001;
-    fast = tmax < 0x1p30 && std::fabs(f.a) + std::fabs(f.b) < 1e300;
+    fast = tmax < 0x1p20 && std::fabs(f.a) + std::fabs(f.b) < 1e300;
   }
   if (fast && !harm) fast = std::fabs(f.a) * xmax < 1e300;
   // 2^-64 folding: onto the factor that multiplies the raw draw
@@ -274,6 +274,16 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
       for (uint32_t j = 0; j < f.dim; ++j) d.width[j] = d.width[j] * kTwoM64;
     }
     p.variant = (unit_dom ? kUnitDomain : 0) | (unit_coef ? kUnitCoef : 0);
+    // NOSHIFT: the argument sweeps >= 0.05 rad over the domain, so the
+    // integrand is far from constant and sum f^2 - (sum f)^2/n does not
+    // cancel; a (near-)constant integrand keeps the shift (exact 0 variance).
+    if (harm) {
+      double sweep = 0.0;
+      for (uint32_t j = 0; j < f.dim; ++j)
+        sweep += std::fabs(f.family == MCB_FAMILY_HARMONIC ? f.k[0] : f.k[j]) *
+                 (f.high[j] - f.low[j]);
+      if (sweep >= 0.05 && std::fabs(f.a) + std::fabs(f.b) > 0.0) p.variant |= kNoShift;
+    }
   } else {
     p.variant = kSafe;
   }
@@ -283,6 +293,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
   const double c = host_eval(f, mid);
   d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
+  if (p.variant & kNoShift) d.shift = 0.0;  // the kernel accumulates f itself
   return p;
 }
 

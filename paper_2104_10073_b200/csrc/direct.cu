@@ -1,12 +1,7 @@
-// direct.cu — the fused direct-MC kernels for sm_100a.
+// direct.cu — launch side of the direct-MC kernels for sm_100a: dispatch
+// table over the fused kernel instantiations (kernels.cuh, direct_*.cu), the
+// tile-table expansion, the ordered combine and the test/measurement hooks.
 //
-// K3 k_direct<FAM,D,V>: one CTA per tile = (integrand, trial, chunk) unit of
-//    <= 65536 samples (reference task, src/batch.cpp:235-253).  Each thread
-//    walks sample pairs: Philox in registers (K1) -> FP64 family value (K2)
-//    -> running sums of g = f - shift and g^2 -> warp butterfly -> fixed
-//    CTA tree -> one TilePartial.  Replaces accumulate_chunk
-//    (src/estimator.cpp:36-49) + ChunkAccum::add (:9-18).  No global memory
-//    traffic besides the descriptor read and a 24-byte partial per tile.
 // K4 k_combine: one thread per (integrand, trial) sums its chunk partials in
 //    ascending chunk order (src/estimator.cpp:55-73 ordering) and forms the
 //    McEstimate fields.  Deterministic: no float atomics anywhere, reduction
@@ -17,7 +12,7 @@
 #include <cmath>
 #include <cstdint>
 
-#include "mcb_internal.hpp"
+#include "kernels.cuh"
 
 namespace mcb {
 namespace detail {
@@ -25,111 +20,6 @@ namespace detail {
 using dev::FnDesc;
 using dev::PhiloxPrefix;
 using dev::TilePartial;
-
-__constant__ dev::SinCosConsts c_sincos = MCB_SINCOS_CONSTS;
-
-__device__ __forceinline__ bool finite64(double x) {
-  // exponent != 0x7FF
-  return (uint32_t(__double2hiint(x)) & 0x7FF00000u) != 0x7FF00000u;
-}
-
-__device__ __forceinline__ double shfl_xor_d(double v, int m) {
-  return __shfl_xor_sync(0xFFFFFFFFu, v, m);
-}
-
-template <int FAM, int D, int V>
-__global__ void __launch_bounds__(kThreads) k_direct(const FnDesc* __restrict__ fns,
-                                                     const uint32_t* __restrict__ tile_fn,
-                                                     uint64_t tile0,
-                                                     TilePartial* __restrict__ part) {
-  constexpr bool UNIT_DOM = (V & kUnitDomain) != 0;
-  constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
-  constexpr bool CHECK = (V & kSafe) != 0;
-
-  const uint64_t tile = tile0 + blockIdx.x;
-  const uint32_t fi = __ldg(tile_fn + tile);
-  const FnDesc& F = fns[fi];
-  const FnDesc f = F;  // uniform; ptxas keeps only the fields this variant reads
-
-  const uint32_t rem = uint32_t(tile - f.tile_base);
-  const uint32_t trial = rem / f.n_chunks;
-  const uint32_t chunk = rem - trial * f.n_chunks;
-  const uint32_t count =
-      (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
-                                : MCB_CHUNK_SIZE;
-  const uint32_t pairs = (count + 1) >> 1;
-  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
-  __shared__ dev::QuadCoef tab[4];
-  if (threadIdx.x < 4) tab[threadIdx.x] = dev::quad_coef(f.a, f.b, int(threadIdx.x));
-  __syncthreads();
-
-  double s1 = 0.0, s2 = 0.0;
-  uint32_t nbad = 0;
-  // Software pipeline: iteration i folds pair q_i's transcendental part
-  // (FP64-heavy) while generating pair q_{i+1} (integer-heavy), so the two
-  // independent streams interleave in one instruction window.  The last
-  // iteration generates one pair past the chunk; it is discarded.
-  const uint32_t iters = threadIdx.x < pairs ? (pairs - threadIdx.x + kThreads - 1) / kThreads : 0u;
-  double a0, a1;
-  dev::gen_pair<FAM, D, UNIT_DOM, CHECK>(f, P, threadIdx.x, a0, a1);
-  for (uint32_t it = 0; it < iters; ++it) {
-    const uint32_t q = threadIdx.x + it * kThreads;
-    double b0, b1;
-    dev::gen_pair<FAM, D, UNIT_DOM, CHECK>(f, P, q + kThreads, b0, b1);
-    const double f0 = dev::finish<FAM, UNIT_COEF, CHECK>(f, c_sincos, tab, a0);
-    const double f1 = dev::finish<FAM, UNIT_COEF, CHECK>(f, c_sincos, tab, a1);
-    a0 = b0;
-    a1 = b1;
-    const bool has1 = 2 * q + 1 < count;
-    double g0 = __dsub_rn(f0, f.shift);
-    double g1 = __dsub_rn(f1, f.shift);
-    if (CHECK) {
-      const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
-      nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
-      g0 = ok0 ? g0 : 0.0;
-      g1 = ok1 ? g1 : 0.0;
-    } else {
-      g1 = has1 ? g1 : 0.0;
-    }
-    s1 = __dadd_rn(s1, g0);
-    s2 = fma(g0, g0, s2);
-    s1 = __dadd_rn(s1, g1);
-    s2 = fma(g1, g1, s2);
-  }
-
-  // fixed-shape reduction: warp butterfly, then warps 0..7 in order
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
-    s1 = __dadd_rn(s1, shfl_xor_d(s1, m));
-    s2 = __dadd_rn(s2, shfl_xor_d(s2, m));
-    if (CHECK) nbad += __shfl_xor_sync(0xFFFFFFFFu, nbad, m);
-  }
-  __shared__ double sh1[kThreads / 32], sh2[kThreads / 32];
-  __shared__ uint32_t shb[kThreads / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    sh1[warp] = s1;
-    sh2[warp] = s2;
-    shb[warp] = nbad;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t1 = sh1[0], t2 = sh2[0];
-    uint32_t tb = shb[0];
-#pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) {
-      t1 = __dadd_rn(t1, sh1[w]);
-      t2 = __dadd_rn(t2, sh2[w]);
-      tb += shb[w];
-    }
-    TilePartial p;
-    p.s1 = t1;
-    p.s2 = t2;
-    p.n_nonfinite = CHECK ? tb : 0u;
-    p.n_finite = count - p.n_nonfinite;
-    part[tile] = p;
-  }
-}
 
 // tile_fn[t] = integrand slot owning tile t (one warp per integrand).
 __global__ void k_expand_tiles(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32_t trials,
@@ -205,25 +95,6 @@ __global__ void k_debug_points(uint32_t key0, uint32_t key1, uint32_t trial, uin
   }
 }
 
-// Family values of the pairs [first_pair, first_pair + n_pairs) of one chunk,
-// through exactly the eval_pair instantiation the fused kernel uses.
-template <int FAM, int D, int V>
-__global__ void k_debug_eval(const FnDesc* __restrict__ fn, uint32_t trial, uint32_t chunk,
-                             uint32_t first_pair, uint32_t n_pairs, double* __restrict__ out) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const FnDesc f = *fn;
-  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, chunk, trial);
-  __shared__ dev::QuadCoef tab[4];
-  if (threadIdx.x < 4) tab[threadIdx.x] = dev::quad_coef(f.a, f.b, int(threadIdx.x));
-  __syncthreads();
-  if (i >= n_pairs) return;
-  double f0, f1;
-  dev::eval_pair<FAM, D, (V & kUnitDomain) != 0, (V & kUnitCoef) != 0, (V & kSafe) != 0>(
-      f, c_sincos, tab, P, first_pair + i, f0, f1);
-  out[2 * uint64_t(i)] = f0;
-  out[2 * uint64_t(i) + 1] = f1;
-}
-
 // Integer-multiply pipe probe: 16 independent 32x32->64 multiply chains per
 // thread (the same mulhilo as Philox, i.e. IMAD.WIDE.U32 by a constant),
 // folded with one LOP3 each like a Philox round.  The result feeds `sink`
@@ -248,56 +119,20 @@ __global__ void __launch_bounds__(256) k_mul_probe(uint32_t* sink, int iters) {
 
 // ---- dispatch -------------------------------------------------------------
 
-using DirectFn = void (*)(const FnDesc*, const uint32_t*, uint64_t, TilePartial*);
-using EvalFn = void (*)(const FnDesc*, uint32_t, uint32_t, uint32_t, uint32_t, double*);
-
-struct Entry {
-  DirectFn direct = nullptr;
-  EvalFn eval = nullptr;
-};
-
-struct Table {
-  Entry e[4][MCB_MAX_DIM + 1][8];
-  template <int FAM, int D, int V>
-  void put() {
-    e[FAM][D][V].direct = k_direct<FAM, D, V>;
-    e[FAM][D][V].eval = k_debug_eval<FAM, D, V>;
-  }
-  template <int FAM, int D>
-  void put_common() {
-    put<FAM, D, 0>();
-    put<FAM, D, kUnitDomain>();
-    put<FAM, D, kSafe>();
-  }
-  template <int D>
-  void put_dim() {
-    put_common<MCB_FAMILY_HARMONIC, D>();
-    put<MCB_FAMILY_HARMONIC, D, kUnitCoef>();
-    put<MCB_FAMILY_HARMONIC, D, kUnitCoef | kUnitDomain>();
-    put_common<MCB_FAMILY_HARMONIC_VEC, D>();
-    if constexpr (D >= 2) put_common<MCB_FAMILY_ABS2, D>();
-    if constexpr (D >= 3) put_common<MCB_FAMILY_ABS3, D>();
-  }
-  Table() {
-    put_dim<1>();
-    put_dim<2>();
-    put_dim<3>();
-    put_dim<4>();
-    put_dim<5>();
-    put_dim<6>();
-    put_dim<7>();
-    put_dim<8>();
-  }
-};
-
 static const Table& table() {
-  static const Table t;
+  static const Table t = [] {
+    Table x;
+    register_harmonic(x);
+    register_harmonic_vec(x);
+    register_abs(x);
+    return x;
+  }();
   return t;
 }
 
 static const Entry* entry(int family, int dim, int variant) {
   if (family < 0 || family > 3 || dim < 1 || dim > int(MCB_MAX_DIM) || variant < 0 ||
-      variant > 7)
+      variant > 15)
     return nullptr;
   const Entry* e = &table().e[family][dim][variant];
   return e->direct ? e : nullptr;

@@ -1,0 +1,197 @@
+// kernels.cuh — the fused direct-MC kernel template (K3) and its test twin.
+//
+// K3 k_direct<FAM,D,V>: one CTA per tile = (integrand, trial, chunk) unit of
+//    <= 65536 samples (the reference task, src/batch.cpp:235-253).  Each
+//    thread walks sample pairs: Philox in registers (K1) -> FP64 family value
+//    (K2) -> running sums of g = f - shift and g^2 -> warp butterfly -> fixed
+//    CTA tree -> one TilePartial.  Replaces accumulate_chunk
+//    (src/estimator.cpp:36-49) + ChunkAccum::add (:9-18).  Global memory
+//    traffic is the descriptor, the 8 KB trig table (L2-resident) and a
+//    24-byte partial per tile.  No float atomics: the reduction shape is
+//    fixed, so results do not depend on scheduling or the GPU count.
+//
+// Included by the per-family translation units (direct_*.cu), which
+// instantiate the (family, dim, variant) combinations and register them in
+// the dispatch table (direct.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mcb_internal.hpp"
+
+namespace mcb {
+namespace detail {
+
+using dev::FnDesc;
+using dev::PhiloxPrefix;
+using dev::TilePartial;
+using dev::TrigAB;
+
+// Reduction / trig constants (constant bank: DFMA takes them as operands).
+static __constant__ dev::TrigConsts c_trig = MCB_TRIG_CONSTS;
+
+__device__ __forceinline__ bool finite64(double x) {
+  return (uint32_t(__double2hiint(x)) & 0x7FF00000u) != 0x7FF00000u;  // exponent != 0x7FF
+}
+
+// Per-CTA A_m/B_m table of the FAST harmonic form (see mcb_device.cuh).
+template <bool UNIT_COEF>
+__device__ __forceinline__ void build_trig_table(TrigAB* ab, double a, double b) {
+  for (int m = threadIdx.x; m < 512; m += blockDim.x)
+    ab[m] = dev::trig_ab<UNIT_COEF>(dev::g_trig_dev[m], a, b);
+}
+
+template <int FAM, int D, int V>
+__global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
+    k_direct(const FnDesc* __restrict__ fns, const uint32_t* __restrict__ tile_fn, uint64_t tile0,
+             TilePartial* __restrict__ part) {
+  constexpr bool UNIT_DOM = (V & kUnitDomain) != 0;
+  constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
+  constexpr bool SAFE = (V & kSafe) != 0;
+  constexpr bool NOSHIFT = (V & kNoShift) != 0;
+  constexpr bool HARM = FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC;
+  constexpr bool TABLE = HARM && !SAFE;
+
+  const uint64_t tile = tile0 + blockIdx.x;
+  const uint32_t fi = __ldg(tile_fn + tile);
+  const FnDesc f = fns[fi];  // uniform; ptxas keeps only the fields this variant reads
+
+  const uint32_t rem = uint32_t(tile - f.tile_base);
+  const uint32_t trial = rem / f.n_chunks;
+  const uint32_t chunk = rem - trial * f.n_chunks;
+  const uint32_t count =
+      (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
+                                : MCB_CHUNK_SIZE;
+  const uint32_t pairs = (count + 1) >> 1;
+  const PhiloxPrefix P =
+      dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
+  __shared__ TrigAB ab[TABLE ? 512 : 1];
+  if (TABLE) {
+    build_trig_table<UNIT_COEF>(ab, f.a, f.b);
+    __syncthreads();
+  }
+
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t nbad = 0;
+  // Software pipeline: iteration i finishes pair q_i (FP64-heavy) while
+  // generating pair q_{i+1} (integer-heavy).  The last iteration generates
+  // one pair past the chunk, which is discarded.  Round-1 Philox products
+  // advance by 64-bit adds: M0 * (q + T) * D = M0 * q * D + M0 * T * D.
+  const uint32_t iters =
+      threadIdx.x < pairs ? (pairs - threadIdx.x + kThreads - 1) / kThreads : 0u;
+  uint64_t pbase = uint64_t(dev::kM0) * uint64_t(threadIdx.x * uint32_t(D));
+  constexpr uint64_t kStep = uint64_t(dev::kM0) * uint64_t(kThreads * D);
+  double a0, a1;
+  dev::gen_pair<FAM, D, UNIT_DOM, SAFE>(f, P, pbase, a0, a1);
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint32_t q = threadIdx.x + it * kThreads;
+    pbase += kStep;
+    double b0, b1;
+    dev::gen_pair<FAM, D, UNIT_DOM, SAFE>(f, P, pbase, b0, b1);
+    const double f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a0);
+    const double f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a1);
+    a0 = b0;
+    a1 = b1;
+    const bool has1 = 2 * q + 1 < count;
+    double g0 = NOSHIFT ? f0 : __dsub_rn(f0, f.shift);
+    double g1 = NOSHIFT ? f1 : __dsub_rn(f1, f.shift);
+    if (SAFE) {
+      const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
+      nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+      g0 = ok0 ? g0 : 0.0;
+      g1 = ok1 ? g1 : 0.0;
+    } else {
+      g1 = has1 ? g1 : 0.0;
+    }
+    s1 = __dadd_rn(s1, g0);
+    s2 = fma(g0, g0, s2);
+    s1 = __dadd_rn(s1, g1);
+    s2 = fma(g1, g1, s2);
+  }
+
+  // fixed-shape reduction: warp butterfly, then warps 0..W-1 in order
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    s1 = __dadd_rn(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, m));
+    s2 = __dadd_rn(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, m));
+    if (SAFE) nbad += __shfl_xor_sync(0xFFFFFFFFu, nbad, m);
+  }
+  __shared__ double sh1[kThreads / 32], sh2[kThreads / 32];
+  __shared__ uint32_t shb[kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sh1[warp] = s1;
+    sh2[warp] = s2;
+    shb[warp] = nbad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t1 = sh1[0], t2 = sh2[0];
+    uint32_t tb = shb[0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) {
+      t1 = __dadd_rn(t1, sh1[w]);
+      t2 = __dadd_rn(t2, sh2[w]);
+      tb += shb[w];
+    }
+    TilePartial p;
+    p.s1 = t1;
+    p.s2 = t2;
+    p.n_nonfinite = SAFE ? tb : 0u;
+    p.n_finite = count - p.n_nonfinite;
+    part[tile] = p;
+  }
+}
+
+// Family values of the pairs [first_pair, first_pair + n_pairs) of one chunk,
+// through exactly the gen_pair/finish instantiation the fused kernel uses.
+template <int FAM, int D, int V>
+__global__ void k_debug_eval(const FnDesc* __restrict__ fn, uint32_t trial, uint32_t chunk,
+                             uint32_t first_pair, uint32_t n_pairs, double* __restrict__ out) {
+  constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
+  constexpr bool SAFE = (V & kSafe) != 0;
+  constexpr bool TABLE =
+      (FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC) && !SAFE;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const FnDesc f = *fn;
+  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, chunk, trial);
+  __shared__ TrigAB ab[TABLE ? 512 : 1];
+  if (TABLE) {
+    build_trig_table<UNIT_COEF>(ab, f.a, f.b);
+    __syncthreads();
+  }
+  if (i >= n_pairs) return;
+  double f0, f1;
+  dev::eval_pair<FAM, D, (V & kUnitDomain) != 0, UNIT_COEF, SAFE>(f, c_trig, ab, P, first_pair + i,
+                                                                   f0, f1);
+  out[2 * uint64_t(i)] = f0;
+  out[2 * uint64_t(i) + 1] = f1;
+}
+
+// ---- dispatch table ----------------------------------------------------------
+
+using DirectFn = void (*)(const FnDesc*, const uint32_t*, uint64_t, TilePartial*);
+using EvalFn = void (*)(const FnDesc*, uint32_t, uint32_t, uint32_t, uint32_t, double*);
+
+struct Entry {
+  DirectFn direct = nullptr;
+  EvalFn eval = nullptr;
+};
+
+struct Table {
+  Entry e[4][MCB_MAX_DIM + 1][16];
+  template <int FAM, int D, int V>
+  void put() {
+    e[FAM][D][V].direct = k_direct<FAM, D, V>;
+    e[FAM][D][V].eval = k_debug_eval<FAM, D, V>;
+  }
+};
+
+void register_harmonic(Table& t);
+void register_harmonic_vec(Table& t);
+void register_abs(Table& t);
+
+}  // namespace detail
+}  // namespace mcb

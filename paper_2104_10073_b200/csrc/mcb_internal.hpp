@@ -13,14 +13,25 @@
 namespace mcb {
 namespace detail {
 
-constexpr int kThreads = 256;  // CTA size of the fused kernel (8 warps)
+#ifndef MCB_THREADS
+#define MCB_THREADS 256
+#endif
+#ifndef MCB_MIN_BLOCKS
+#define MCB_MIN_BLOCKS 1
+#endif
+#ifndef MCB_PIPELINE
+#define MCB_PIPELINE 1
+#endif
+constexpr int kThreads = MCB_THREADS;  // CTA size of the fused kernel
 
 enum Variant : int {
   kUnitDomain = 1,  // low == 0, width == 1 on every axis
   kUnitCoef = 2,    // HARMONIC with a == b == 1 (Fig.1 source form)
-  kSafe = 4         // plain parameters, libdevice sincos, non-finite samples
+  kSafe = 4,        // plain parameters, libdevice sincos, non-finite samples
                     // counted and skipped (used when the host cannot prove
-                    // the FAST preconditions, see capi.cpp choose_variant)
+                    // the FAST preconditions, see capi.cpp prepare())
+  kNoShift = 8      // harmonic FAST: accumulate f itself (the host proved the
+                    // integrand far from constant, so no cancellation)
 };
 
 // One kernel launch = one (family, dim, variant) group of integrands whose

@@ -7,9 +7,9 @@
 //  2. u_scaled(hi, lo) * 2^-64 == to_unit_double(hi, lo) bit-exactly
 //     (src/sampling.cpp:72-75)
 //  3. the 2^-64 folding used by the FAST variants is bit-exact
-//  4. sincos_fast is within 2 ulp of the correctly rounded sin/cos
-//  5. the quadrant-coefficient form of a*cos + b*sin is bit-identical to the
-//     literal expression evaluated with the same sin/cos values
+//  4. the table-form sin/cos (the kernel's reduction): absolute error < 3 * 2^-53
+//  5. a*cos t + b*sin t in table form: error < 2.5 * max(|a|,|b|) * 2^-52
+//  6. trig_table.inc holds correctly rounded cos/sin of m*pi/256
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -42,12 +42,6 @@ static uint64_t bits(double x) {
   uint64_t b;
   std::memcpy(&b, &x, 8);
   return b;
-}
-
-static double ulp_err(double got, long double exact) {
-  const double e = double(exact);
-  const double ulp = std::nextafter(std::fabs(e), INFINITY) - std::fabs(e);
-  return double(std::fabs((long double)got - exact)) / ulp;
 }
 
 int main() {
@@ -88,36 +82,48 @@ int main() {
     const double lo = double(int64_t(rng() % 2001) - 1000) * 0.37;
     CHECK(bits(lo + (w * kTwoM64) * v[0]) == bits(lo + w * u[0]), "fold w=%a", w);
   }
-  // 4. sincos_fast accuracy
-  const SinCosConsts K = MCB_SINCOS_CONSTS;
+  // 4. table-form sin/cos accuracy (same reduction as the kernel)
+  const TrigConsts K = MCB_TRIG_CONSTS;
   double max_s = 0, max_c = 0;
-  for (int e = -3; e <= 20; ++e) {
+  for (int e = -3; e <= 19; ++e) {
     std::uniform_real_distribution<double> U(-std::ldexp(1.0, e), std::ldexp(1.0, e));
     for (int i = 0; i < 200000; ++i) {
       const double t = U(rng);
       double s, c;
-      sincos_fast(K, t, s, c);
-      max_s = std::fmax(max_s, ulp_err(s, sinl((long double)t)));
-      max_c = std::fmax(max_c, ulp_err(c, cosl((long double)t)));
+      sincos_table(K, g_trig_host, t, s, c);
+      max_s = std::fmax(max_s, double(std::fabs((long double)s - sinl((long double)t))) / 0x1p-53);
+      max_c = std::fmax(max_c, double(std::fabs((long double)c - cosl((long double)t))) / 0x1p-53);
     }
   }
-  std::printf("sincos_fast max error: sin %.3f ulp, cos %.3f ulp\n", max_s, max_c);
-  CHECK(max_s < 2.0 && max_c < 2.0, "sincos accuracy sin %.3f cos %.3f", max_s, max_c);
-  // 5. quadrant-coefficient identity
-  for (int i = 0; i < 1000000; ++i) {
+  // absolute error in units of 2^-53 (half an ulp of 1): what a Monte Carlo
+  // mean sees; glibc's correctly rounded sin/cos are within 1 of these units
+  std::printf("table sin/cos max abs error: sin %.3f, cos %.3f x 2^-53\n", max_s, max_c);
+  CHECK(max_s < 3.0 && max_c < 3.0, "sincos accuracy sin %.3f cos %.3f", max_s, max_c);
+  // 5. harmonic value a*cos t + b*sin t in table form vs correctly rounded,
+  //    in units of the coefficient scale max(|a|,|b|) * 2^-52
+  double max_h = 0, max_u = 0;
+  for (int i = 0; i < 2000000; ++i) {
     const double t = std::uniform_real_distribution<double>(-700, 700)(rng);
     const double a = std::uniform_real_distribution<double>(-3, 3)(rng);
     const double b = std::uniform_real_distribution<double>(-3, 3)(rng);
-    double sf, cf, s, c;
-    uint32_t q;
-    sincos_fast(K, t, sf, cf);
-    sincos_core(K, t, s, c, q);
-    const QuadCoef ab = quad_coef(a, b, int(q & 3u));
-    const double lit = (a * cf) + (b * sf);
-    const double quad = (ab.A * c) + (ab.B * s);
-    CHECK(bits(lit) == bits(quad), "quad a=%a b=%a t=%a", a, b, t);
-    const QuadCoef one = quad_coef(1.0, 1.0, int(q & 3u));
-    CHECK(bits(cf + sf) == bits(std::fma(one.A, c, one.B * s)), "unit quad t=%a", t);
+    double r, s, c;
+    uint32_t m;
+    trig_reduce(K, t, r, m);
+    trig_sc(K, r, s, c);
+    const double h = trig_combine(trig_ab<false>(g_trig_host[m], a, b), s, c);
+    const long double ex = (long double)a * cosl((long double)t) + (long double)b * sinl((long double)t);
+    max_h = std::fmax(max_h, double(std::fabs((long double)h - ex)) / (std::fmax(std::fabs(a), std::fabs(b)) * 0x1p-52));
+    const double u = trig_combine(trig_ab<true>(g_trig_host[m], 1.0, 1.0), s, c);
+    const long double exu = cosl((long double)t) + sinl((long double)t);
+    max_u = std::fmax(max_u, double(std::fabs((long double)u - exu)) / 0x1p-52);
+  }
+  std::printf("a cos t + b sin t: max error %.3f x max(|a|,|b|) 2^-52; unit form %.3f x 2^-52\n", max_h, max_u);
+  CHECK(max_h < 2.5 && max_u < 2.0, "harmonic value accuracy %.3f %.3f", max_h, max_u);
+  // 6. the table itself: entries equal the correctly rounded cos/sin
+  for (int mm = 0; mm < 512; ++mm) {
+    const long double ang = (long double)mm * 3.14159265358979323846264338327950288L / 256.0L;
+    CHECK(std::fabs((long double)g_trig_host[mm].c - cosl(ang)) <= 0x1p-53, "table c %d", mm);
+    CHECK(std::fabs((long double)g_trig_host[mm].s - sinl(ang)) <= 0x1p-53, "table s %d", mm);
   }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
