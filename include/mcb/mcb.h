@@ -186,9 +186,10 @@ MCB_API mcb_status mcb_debug_points(uint64_t seed, uint32_t integrand_index, uin
 MCB_API mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
                           uint64_t chunk, uint64_t first_point, uint64_t count,
                           int device, double* out);
-/* Microbenchmark of the integer multiply pipe that bounds Philox:
- * 32x32->64 multiplies per second on `device` over ~`ms` milliseconds. */
-MCB_API mcb_status mcb_probe_mul_peak(int device, double ms, double* muls_per_s);
+/* Roofline probe: Philox4x32-10 blocks per second that `device` can generate
+ * with no integrand work at all (same generator code as the fused kernel),
+ * timed over ~`ms` milliseconds.  The denominator of bench.py's roofline. */
+MCB_API mcb_status mcb_probe_philox_peak(int device, double ms, double* blocks_per_s);
 
 #ifdef __cplusplus
 }

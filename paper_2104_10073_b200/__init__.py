@@ -82,7 +82,7 @@ ABI_SYMBOLS = [
     "mcb_to_dsl", "mcb_validate", "mcb_partition", "mcb_summarize_trials", "mcb_run_direct",
     "mcb_direct_mc", "mcb_plan_create", "mcb_plan_launch", "mcb_plan_download",
     "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
-    "mcb_probe_mul_peak",
+    "mcb_probe_philox_peak",
 ]
 
 
@@ -114,7 +114,7 @@ def _load() -> ctypes.CDLL:
         "mcb_plan_destroy": (None, [vp]),
         "mcb_debug_points": (i32, [u64, u32, u32, u64, u64, u64, u32, P(dbl), P(dbl), i32, vp]),
         "mcb_debug_eval": (i32, [P(Integrand), u64, u32, u64, u64, u64, i32, vp]),
-        "mcb_probe_mul_peak": (i32, [i32, dbl, P(dbl)]),
+        "mcb_probe_philox_peak": (i32, [i32, dbl, P(dbl)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -294,9 +294,10 @@ def debug_eval(f: Integrand, seed: int, trial: int, chunk: int, first_point: int
     return out
 
 
-def probe_mul_peak(device: int = 0, ms: float = 20.0) -> float:
+def probe_philox_peak(device: int = 0, ms: float = 50.0) -> float:
+    """Philox4x32-10 blocks/s the device generates with no integrand work."""
     v = ctypes.c_double()
-    _check(lib.mcb_probe_mul_peak(device, ms, ctypes.byref(v)))
+    _check(lib.mcb_probe_philox_peak(device, ms, ctypes.byref(v)))
     return v.value
 
 

@@ -95,25 +95,27 @@ __global__ void k_debug_points(uint32_t key0, uint32_t key1, uint32_t trial, uin
   }
 }
 
-// Integer-multiply pipe probe: 16 independent 32x32->64 multiply chains per
-// thread (the same mulhilo as Philox, i.e. IMAD.WIDE.U32 by a constant),
-// folded with one LOP3 each like a Philox round.  The result feeds `sink`
-// so nothing is dead code.
-__global__ void __launch_bounds__(256) k_mul_probe(uint32_t* sink, int iters) {
-  uint32_t x[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) x[i] = threadIdx.x * 2654435761u + i * 40503u + blockIdx.x;
+// Philox-generation roofline probe: Philox4x32-10 blocks with nothing else
+// (4 independent blocks per thread per iteration, the same philox_block_p and
+// incremental round-1 products as the fused kernel, outputs XOR-folded so
+// nothing is dead code).  On B200 the IMAD.WIDE multiplies of Philox run on
+// the FP64 pipe, which also executes the integrand's FP64 work, so this is
+// the ceiling for any sampler that must produce these exact streams.
+__global__ void __launch_bounds__(256) k_philox_probe(const uint32_t* __restrict__ key,
+                                                      uint32_t* sink, int iters) {
+  const PhiloxPrefix P = dev::make_prefix(key[0], key[1], blockIdx.x & 15u, blockIdx.x >> 4);
+  uint64_t pbase = uint64_t(dev::kM0) * uint64_t(threadIdx.x * 4u);
+  constexpr uint64_t kStep = uint64_t(dev::kM0) * 1024u;
+  uint32_t acc = 0;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      uint32_t hi, lo;
-      dev::mulhilo(i & 1 ? dev::kM1 : dev::kM0, x[i], hi, lo);
-      x[i] = hi ^ lo;
+    for (int i = 0; i < 4; ++i) {
+      uint32_t o[4];
+      dev::philox_block_p(P, pbase + uint64_t(i) * dev::kM0, o);
+      acc ^= o[0] ^ o[1] ^ o[2] ^ o[3];
     }
+    pbase += kStep;
   }
-  uint32_t acc = 0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) acc ^= x[i];
   if (acc == 0x12345678u) sink[blockIdx.x] = acc;
 }
 
@@ -193,8 +195,9 @@ cudaError_t launch_debug_eval_impl(int family, int dim, int variant, const FnDes
   return cudaGetLastError();
 }
 
-cudaError_t launch_mul_probe(uint32_t* sink, int n_ctas, int iters, cudaStream_t s) {
-  k_mul_probe<<<n_ctas, 256, 0, s>>>(sink, iters);
+cudaError_t launch_philox_probe(const uint32_t* key, uint32_t* sink, int n_ctas, int iters,
+                               cudaStream_t s) {
+  k_philox_probe<<<n_ctas, 256, 0, s>>>(key, sink, iters);
   return cudaGetLastError();
 }
 

@@ -58,7 +58,8 @@ cudaError_t launch_debug_points(uint32_t key0, uint32_t key1, uint32_t trial, ui
 cudaError_t launch_debug_eval_impl(int family, int dim, int variant, const dev::FnDesc* fn,
                                    uint32_t trial, uint32_t chunk, uint32_t first_pair,
                                    uint32_t n_pairs, double* out, cudaStream_t s);
-cudaError_t launch_mul_probe(uint32_t* sink, int n_ctas, int iters, cudaStream_t s);
+cudaError_t launch_philox_probe(const uint32_t* key, uint32_t* sink, int n_ctas, int iters,
+                               cudaStream_t s);
 
 }  // namespace detail
 }  // namespace mcb
