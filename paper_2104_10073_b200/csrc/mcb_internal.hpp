@@ -17,7 +17,7 @@ namespace detail {
 #define MCB_THREADS 256
 #endif
 #ifndef MCB_MIN_BLOCKS
-#define MCB_MIN_BLOCKS 1
+#define MCB_MIN_BLOCKS 2
 #endif
 #ifndef MCB_PIPELINE
 #define MCB_PIPELINE 1

@@ -1,0 +1,70 @@
+#!/usr/bin/env python
+"""Throughput of every BASELINE.json config on one GPU (device-resident plan,
+CUDA events on the launching stream).  Not the driver's bench line (that is
+bench.py on configs[1]); this is the per-config table for DESIGN.md.
+
+  python tools/bench_configs.py [--reps 3] [--configs c1,c2,c3,c4,c5] [--c5-fns 10000]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--c5-fns", type=int, default=10000)
+    ap.add_argument("--c4-trials", type=int, default=10)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2104_10073_b200 as mcb
+    from paper_2104_10073_b200 import workloads as w
+
+    builders = {
+        "c1": lambda: w.c1(),
+        "c2": lambda: w.c2(),
+        "c3": lambda: w.c3(),
+        "c4": lambda: w.c4(trials=args.c4_trials),
+        "c5": lambda: w.c5(n_fns=args.c5_fns),
+    }
+    stream = torch.cuda.current_stream()
+    peak = mcb.probe_philox_peak(0, 50.0)
+    out = {"philox_peak_blocks_per_s": peak}
+    for name in args.configs.split(","):
+        fns, seed, trials = builders[name]()
+        plan = mcb.Plan(fns, seed, trials)
+        info = plan.info()
+        plan.launch(stream.cuda_stream)  # warm-up (module load)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            plan.launch(stream.cuda_stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b) * 1e-3)
+        t = min(times)
+        res = plan.download(stream.cuda_stream)
+        plan.close()
+        ok = int((res["status"] == mcb.TRIAL_OK).sum())
+        out[name] = {"integrands": len(fns), "trials": trials, "samples": info.total_samples,
+                     "groups": info.n_groups, "tiles": info.n_tiles, "seconds": t,
+                     "samples_per_s": info.total_samples / t,
+                     "philox_blocks_per_s": info.philox_blocks / t,
+                     "frac_of_philox_peak": info.philox_blocks / t / peak,
+                     "ok_trials": ok}
+        print(name, json.dumps(out[name]), flush=True)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
