@@ -63,8 +63,16 @@ typedef enum mcb_family {
   MCB_FAMILY_HARMONIC = 0,
   MCB_FAMILY_HARMONIC_VEC = 1,
   MCB_FAMILY_ABS2 = 2,
-  MCB_FAMILY_ABS3 = 3
+  MCB_FAMILY_ABS3 = 3,
+  MCB_FAMILY_PROGRAM = 4 /* any DSL source: compiled by mcb_program_compile, run by
+                            the GPU interpreter (ref/src/expr.cpp:520-553 semantics) */
 } mcb_family;
+
+/* Maximum number of parameters a PROGRAM integrand binds (values in k[]). */
+#define MCB_MAX_PARAMS 8u
+
+/* A compiled DSL program (opaque; immutable, shareable across threads). */
+typedef struct mcb_program mcb_program;
 
 #define MCB_FLAG_UNIT_COEFFS 0x1u
 
@@ -80,9 +88,11 @@ typedef struct mcb_integrand {
   uint32_t flags;           /* MCB_FLAG_* */
   uint64_t n_samples;       /* per trial, >= 2 */
   double a, b;              /* coefficients (ABS families use `a`) */
-  double k[MCB_MAX_DIM];    /* HARMONIC: k[0]; HARMONIC_VEC: k[0..dim-1] */
+  double k[MCB_MAX_DIM];    /* HARMONIC: k[0]; HARMONIC_VEC: k[0..dim-1];
+                               PROGRAM: parameter values in sorted-name order */
   double low[MCB_MAX_DIM];  /* HyperRect low  (include/mcbatch/sampling.hpp:14-24) */
   double high[MCB_MAX_DIM]; /* HyperRect high */
+  const mcb_program* program; /* PROGRAM family only (not owned) */
 } mcb_integrand;
 
 enum { MCB_TRIAL_OK = 0, MCB_TRIAL_ALL_NONFINITE = 1 };
@@ -133,6 +143,25 @@ MCB_API mcb_status mcb_partition(const mcb_integrand* fns, size_t n_fns, uint32_
 /* summarize_trials (src/estimator.cpp:320-337) over the OK trials in order. */
 MCB_API mcb_status mcb_summarize_trials(const mcb_trial_stats* per_trial, uint32_t n_trials,
                                 double* mean, double* trial_stddev, uint32_t* n_ok);
+
+/* ---- DSL programs (MCB_FAMILY_PROGRAM) ------------------------------------- */
+/* parse + compile (ref/src/expr.cpp:302-309 parse, :507-518 compile) of
+ * `source` for `dim` coordinates and the given parameter names (any order;
+ * bound in sorted order as the reference does, src/batch.cpp:129-140).
+ * Errors: MCB_ERR_VALIDATION with the reference's wording in mcb_last_error
+ * ("expression does not parse: ...", "x3 exceeds dim=2", "unbound parameter
+ * 'q'"), or when the program exceeds the interpreter's limits (16 stack
+ * slots, 1024 instructions, 512 constants, MCB_MAX_PARAMS parameters). */
+MCB_API mcb_status mcb_program_compile(const char* source, uint32_t dim,
+                                       const char* const* param_names, size_t n_params,
+                                       mcb_program** out);
+MCB_API void mcb_program_destroy(mcb_program* program);
+/* n_instr, stack depth, n_params (each may be NULL). */
+MCB_API mcb_status mcb_program_info(const mcb_program* program, uint32_t* n_instr,
+                                    uint32_t* depth, uint32_t* n_params);
+/* i-th bound parameter name in binding (sorted) order; returns bytes needed incl. NUL. */
+MCB_API size_t mcb_program_param_name(const mcb_program* program, uint32_t i, char* buf,
+                                      size_t cap);
 
 /* ---- the hot path -------------------------------------------------------- */
 /* run_batch Direct branch (src/batch.cpp:195-333): every integrand, every

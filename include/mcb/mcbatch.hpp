@@ -4,9 +4,11 @@
 //
 // Differences from the reference, all deliberate:
 //  * IntegrandSpec carries a family descriptor (`family` + `params` map using
-//    the DSL parameter names a, b, k, k1..kd) instead of free DSL source;
-//    `source()` returns the exact DSL the reference would parse, and
-//    `IntegrandSpec::from_source()` recognises those sources.
+//    the DSL parameter names a, b, k, k1..kd); `source()` returns the exact
+//    DSL the reference would parse.  Any other DSL source runs as
+//    Family::Program (GPU interpreter, same sampler and reduction);
+//    `IntegrandSpec::from_source()` picks the family when the source is one
+//    of them and Program otherwise, so reference IntegrandSpecs port as-is.
 //  * JobSpec::workers (CPU threads) becomes JobSpec::devices (CUDA ordinals).
 //    Results are byte-identical for any device list, the analogue of the
 //    reference's worker invariance (tests/test_batch.cpp:91-121).
@@ -67,7 +69,8 @@ enum class Family {
   Harmonic = MCB_FAMILY_HARMONIC,         // a*cos(k*(x1+..+xd)) + b*sin(k*(x1+..+xd))
   HarmonicVec = MCB_FAMILY_HARMONIC_VEC,  // a*cos(k1*x1+..+kd*xd) + b*sin(...)
   Abs2 = MCB_FAMILY_ABS2,                 // a*abs(x1+x2)
-  Abs3 = MCB_FAMILY_ABS3                  // a*abs(x1+x2-x3)
+  Abs3 = MCB_FAMILY_ABS3,                 // a*abs(x1+x2-x3)
+  Program = MCB_FAMILY_PROGRAM            // any DSL source (`program_source`)
 };
 
 enum class Method { Direct };
@@ -83,11 +86,12 @@ struct IntegrandSpec {
   std::map<std::string, double> params;  // a, b, k | a, b, k1..kd | a
   std::uint64_t n_samples = 10000;
   Method method = Method::Direct;
+  std::string program_source;  // Family::Program: the DSL source
 
   // Exact reference DSL source of this descriptor.
   std::string source() const;
-  // Recognise a reference DSL source of one of the families (whitespace
-  // insensitive); throws std::invalid_argument for anything else.
+  // A reference IntegrandSpec: a built-in family when `source` is one of
+  // their DSL forms (whitespace insensitive), else Family::Program.
   static IntegrandSpec from_source(std::string name, const std::string& source, std::size_t dim,
                                    HyperRect domain, std::map<std::string, double> params,
                                    std::uint64_t n_samples);
@@ -183,6 +187,21 @@ double analytic_harmonic(std::uint32_t n);
 JobSpec make_harmonic_job(std::uint32_t n_count, std::uint64_t samples);
 
 // Lowering to the C-ABI descriptor (integrand_index = list position).
-mcb_integrand to_descriptor(const IntegrandSpec& spec, std::uint32_t integrand_index);
+// Family::Program needs a compiled program (see compile_program).
+mcb_integrand to_descriptor(const IntegrandSpec& spec, std::uint32_t integrand_index,
+                            const mcb_program* program = nullptr);
+
+// Compiled DSL program shared by Program integrands (RAII over mcb_program).
+struct CompiledSource {
+  mcb_program* handle = nullptr;
+  CompiledSource() = default;
+  CompiledSource(const CompiledSource&) = delete;
+  CompiledSource& operator=(const CompiledSource&) = delete;
+  CompiledSource(CompiledSource&& o) noexcept : handle(o.handle) { o.handle = nullptr; }
+  ~CompiledSource() { mcb_program_destroy(handle); }
+};
+// Throws std::invalid_argument with the reference's validation wording.
+CompiledSource compile_program(const std::string& source, std::size_t dim,
+                               const std::map<std::string, double>& params);
 
 }  // namespace mcb

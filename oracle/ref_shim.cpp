@@ -199,6 +199,56 @@ int ref_harmonic_job(std::uint32_t n_count, std::uint64_t samples, double* k_out
   }
 }
 
+// evaluate (src/expr.cpp:520-553) of an arbitrary source with named params.
+int ref_eval_source(const char* source, std::uint32_t dim, const char* const* names,
+                    const double* values, std::size_t n_params, const double* pts,
+                    std::uint64_t n, double* out) {
+  try {
+    std::map<std::string, double> pm;
+    for (std::size_t i = 0; i < n_params; ++i) pm[names[i]] = values[i];
+    std::vector<std::string> nm;
+    std::vector<double> vals;
+    for (auto& [k, v] : pm) { nm.push_back(k); vals.push_back(v); }
+    CompiledProgram prog = compile(parse(source), dim, nm);
+    std::vector<double> stack;
+    for (std::uint64_t i = 0; i < n; ++i) out[i] = prog.evaluate({pts + i * dim, dim}, vals, stack);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// direct_mc (src/estimator.cpp:75-92) of an arbitrary source.
+int ref_direct_mc_source(const char* source, std::uint32_t dim, const char* const* names,
+                         const double* values, std::size_t n_params, const double* lo,
+                         const double* hi, std::uint64_t n_samples, std::uint64_t seed,
+                         std::uint32_t index, std::uint32_t trial, std::uint64_t chunk_base,
+                         mcb_trial_stats* out) {
+  try {
+    std::map<std::string, double> pm;
+    for (std::size_t i = 0; i < n_params; ++i) pm[names[i]] = values[i];
+    std::vector<std::string> nm;
+    std::vector<double> vals;
+    for (auto& [k, v] : pm) { nm.push_back(k); vals.push_back(v); }
+    CompiledProgram prog = compile(parse(source), dim, nm);
+    std::memset(out, 0, sizeof *out);
+    try {
+      fill(direct_mc(prog, vals, rect_of(dim, lo, hi), n_samples,
+                     StreamKey{seed, index, trial, chunk_base}),
+           out);
+    } catch (const AllSamplesNonFinite&) {
+      out->status = MCB_TRIAL_ALL_NONFINITE;
+      out->n_samples = n_samples;
+      out->n_nonfinite = n_samples;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 double ref_harmonic_closed_form(double k) { return harmonic_closed_form(k); }
 double ref_analytic_harmonic(std::uint32_t n) { return analytic_harmonic(n); }
 

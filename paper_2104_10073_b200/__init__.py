@@ -30,7 +30,9 @@ FAMILY_HARMONIC = 0
 FAMILY_HARMONIC_VEC = 1
 FAMILY_ABS2 = 2
 FAMILY_ABS3 = 3
+FAMILY_PROGRAM = 4
 FLAG_UNIT_COEFFS = 1
+MAX_PARAMS = 8
 
 TRIAL_OK = 0
 TRIAL_ALL_NONFINITE = 1
@@ -51,7 +53,7 @@ class Integrand(ctypes.Structure):
                 ("integrand_index", ctypes.c_uint32), ("flags", ctypes.c_uint32),
                 ("n_samples", ctypes.c_uint64), ("a", ctypes.c_double), ("b", ctypes.c_double),
                 ("k", ctypes.c_double * MAX_DIM), ("low", ctypes.c_double * MAX_DIM),
-                ("high", ctypes.c_double * MAX_DIM)]
+                ("high", ctypes.c_double * MAX_DIM), ("program", ctypes.c_void_p)]
 
 
 class TrialStats(ctypes.Structure):
@@ -82,7 +84,8 @@ ABI_SYMBOLS = [
     "mcb_to_dsl", "mcb_validate", "mcb_partition", "mcb_summarize_trials", "mcb_run_direct",
     "mcb_direct_mc", "mcb_plan_create", "mcb_plan_launch", "mcb_plan_download",
     "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
-    "mcb_probe_philox_peak",
+    "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
+    "mcb_program_param_name",
 ]
 
 
@@ -115,6 +118,10 @@ def _load() -> ctypes.CDLL:
         "mcb_debug_points": (i32, [u64, u32, u32, u64, u64, u64, u32, P(dbl), P(dbl), i32, vp]),
         "mcb_debug_eval": (i32, [P(Integrand), u64, u32, u64, u64, u64, i32, vp]),
         "mcb_probe_philox_peak": (i32, [i32, dbl, P(dbl)]),
+        "mcb_program_compile": (i32, [ctypes.c_char_p, u32, P(ctypes.c_char_p), sz, P(vp)]),
+        "mcb_program_destroy": (None, [vp]),
+        "mcb_program_info": (i32, [vp, P(u32), P(u32), P(u32)]),
+        "mcb_program_param_name": (sz, [vp, u32, ctypes.c_char_p, sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -162,6 +169,53 @@ def harmonic(k: float, dim: int = 4, *, a: float = 1.0, b: float = 1.0, unit_coe
         unit_coeffs = (a == 1.0 and b == 1.0)
     return make_integrand(FAMILY_HARMONIC, dim, k=k, a=a, b=b, low=low, high=high,
                           n_samples=n_samples, index=index, unit_coeffs=unit_coeffs)
+
+
+class Program:
+    """A compiled DSL integrand (``mcb_program_compile``): the reference's
+    source language (ref/src/expr.cpp), run on the GPU by the interpreter
+    kernel.  Parameters bind in sorted-name order; keep the object alive while
+    integrands reference it."""
+
+    def __init__(self, source: str, dim: int, param_names: Sequence[str] = ()):
+        names = sorted(set(param_names))
+        arr = (ctypes.c_char_p * max(1, len(names)))(*[n.encode() for n in names])
+        h = ctypes.c_void_p()
+        _check(lib.mcb_program_compile(source.encode(), dim, arr, len(names), ctypes.byref(h)))
+        self._h = h
+        self.source, self.dim = source, dim
+        n_instr, depth, n_params = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        _check(lib.mcb_program_info(h, ctypes.byref(n_instr), ctypes.byref(depth), ctypes.byref(n_params)))
+        self.n_instr, self.depth = n_instr.value, depth.value
+        self.param_names = []
+        for i in range(n_params.value):
+            buf = ctypes.create_string_buffer(lib.mcb_program_param_name(h, i, None, 0))
+            lib.mcb_program_param_name(h, i, buf, len(buf))
+            self.param_names.append(buf.value.decode())
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def integrand(self, params: Optional[Dict[str, float]] = None, *, low=None, high=None,
+                  n_samples: int = 10000, index: int = 0) -> Integrand:
+        params = params or {}
+        missing = [n for n in self.param_names if n not in params]
+        if missing:
+            raise ValueError(f"unbound parameter '{missing[0]}'")
+        f = make_integrand(FAMILY_PROGRAM, self.dim, k=[params[n] for n in self.param_names] or 0.0,
+                           low=low, high=high, n_samples=n_samples, index=index)
+        f.program = self._h.value
+        f.a = f.b = 0.0
+        return f
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.mcb_program_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def to_dsl(f: Integrand) -> str:

@@ -28,6 +28,13 @@
 
 #include "mcb/mcb.h"
 #include "mcb_internal.hpp"
+#include "program.hpp"
+
+// Opaque compiled program of the C-ABI.
+struct mcb_program {
+  mcb::prog::Program p;
+  std::vector<uint32_t> words;
+};
 
 using mcb::detail::GroupLaunch;
 using mcb::dev::FnDesc;
@@ -65,7 +72,7 @@ uint32_t min_dim(uint32_t family) {
   return family == MCB_FAMILY_ABS2 ? 2u : (family == MCB_FAMILY_ABS3 ? 3u : 1u);
 }
 
-bool family_known(uint32_t f) { return f <= MCB_FAMILY_ABS3; }
+bool family_known(uint32_t f) { return f <= MCB_FAMILY_PROGRAM; }
 
 // Per-sample cost estimate (relative units) for LPT sharding: Philox blocks
 // dominate (d/2 per sample), a sincos costs about one block.
@@ -74,6 +81,8 @@ double sample_cost(const mcb_integrand& f) {
   if (f.family == MCB_FAMILY_ABS2) blocks = std::min(blocks, 1.0);
   if (f.family == MCB_FAMILY_ABS3) blocks = std::min(blocks, 1.5);
   const bool harm = f.family == MCB_FAMILY_HARMONIC || f.family == MCB_FAMILY_HARMONIC_VEC;
+  if (f.family == MCB_FAMILY_PROGRAM)  // interpreter: ~1 block-equivalent per 2 instructions
+    return blocks + (f.program ? 0.5 * double(f.program->p.code.size()) : 1.0);
   return blocks + (harm ? 1.0 : 0.2);
 }
 
@@ -106,6 +115,8 @@ double host_eval(const mcb_integrand& f, const double* x) {
       const double s = x[0] + x[1];
       return f.a * std::fabs(s - x[2]);
     }
+    case MCB_FAMILY_PROGRAM:
+      return f.program ? mcb::prog::evaluate(f.program->p, x, f.k) : 0.0;
   }
   return 0.0;
 }
@@ -145,6 +156,9 @@ std::string to_dsl(const mcb_integrand& f) {
     case MCB_FAMILY_ABS3:
       s = f.a == 1.0 ? "abs(x1+x2-x3)" : "a*abs(x1+x2-x3)";  // tests/test_batch.cpp:51
       break;
+    case MCB_FAMILY_PROGRAM:
+      s = f.program ? f.program->p.source : "";
+      break;
     default:
       s = "";
   }
@@ -171,6 +185,12 @@ void violations_of(const mcb_integrand& f, uint32_t trials,
   if (!family_known(f.family)) {
     out.push_back("unknown integrand family " + std::to_string(f.family));
     return;
+  }
+  if (f.family == MCB_FAMILY_PROGRAM) {
+    if (!f.program) out.push_back("program family needs a compiled program");
+    else if (f.program->p.dim != f.dim)
+      out.push_back("program compiled for dim=" + std::to_string(f.program->p.dim) +
+                    " but the integrand has dim=" + std::to_string(f.dim));
   }
   if (f.dim < 1) out.push_back("dim must be >= 1");
   if (f.dim > MCB_MAX_DIM)
@@ -244,6 +264,16 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   }
   if (f.family == MCB_FAMILY_HARMONIC) finite = finite && std::isfinite(f.k[0]);
   const bool unit_coef = (f.flags & MCB_FLAG_UNIT_COEFFS) != 0;
+  if (f.family == MCB_FAMILY_PROGRAM) {
+    // interpreter: plain parameters, unscaled draws, non-finite counting
+    for (uint32_t j = 0; j < MCB_MAX_DIM; ++j) d.k[j] = f.k[j];
+    p.variant = kSafe | (unit_dom ? kUnitDomain : 0);
+    double mid[MCB_MAX_DIM];
+    for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
+    const double c = host_eval(f, mid);
+    d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
+    return p;
+  }
   const bool harm = f.family == MCB_FAMILY_HARMONIC || f.family == MCB_FAMILY_HARMONIC_VEC;
 
   bool fast = finite && std::isfinite(xmax);
@@ -377,6 +407,8 @@ uint64_t blocks_per_pair(uint32_t family, uint32_t dim) {
 struct HostPlan {
   std::vector<FnDesc> descs;  // group order
   std::vector<GroupLaunch> groups;
+  std::vector<uint32_t> code;  // PROGRAM family: all distinct programs' words
+  std::vector<double> consts;  //   and constant pools
   uint64_t n_tiles = 0, total_samples = 0, philox_blocks = 0;
 };
 
@@ -392,6 +424,7 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     return kx < ky;
   });
   hp.descs.resize(n_fns);
+  std::map<const mcb_program*, std::pair<uint32_t, uint32_t>> prog_at;  // code, const offsets
   uint64_t tile = 0;
   for (size_t r = 0; r < n_fns; ++r) {
     const size_t i = order[r];
@@ -400,10 +433,26 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     d.out_slot = i;
     const uint64_t nt = uint64_t(d.n_chunks) * trials;
     const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
+    uint32_t slots = 0;
+    if (fam == MCB_FAMILY_PROGRAM) {
+      const mcb_program* pg = fns[i].program;
+      auto it = prog_at.find(pg);
+      if (it == prog_at.end()) {
+        it = prog_at.emplace(pg, std::make_pair(uint32_t(hp.code.size()), uint32_t(hp.consts.size()))).first;
+        hp.code.insert(hp.code.end(), pg->words.begin(), pg->words.end());
+        hp.consts.insert(hp.consts.end(), pg->p.consts.begin(), pg->p.consts.end());
+      }
+      d.prog_off = it->second.first;
+      d.prog_len = uint32_t(pg->words.size());
+      d.const_off = it->second.second;
+      d.n_consts = uint32_t(pg->p.consts.size());
+      slots = pg->p.depth;
+    }
     if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
         hp.groups.back().variant != var)
-      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0});
+      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0});
     hp.groups.back().n_tiles += nt;
+    hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
     tile += nt;
     hp.descs[r] = d;
     hp.total_samples += fns[i].n_samples * trials;
@@ -412,7 +461,7 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     hp.philox_blocks += pairs * blocks_per_pair(fns[i].family, fns[i].dim) * trials;
   }
   for (const auto& g : hp.groups)
-    if (!mcb::detail::variant_supported(g.family, g.dim, g.variant))
+    if (g.family != MCB_FAMILY_PROGRAM && !mcb::detail::variant_supported(g.family, g.dim, g.variant))
       return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
   hp.n_tiles = tile;
   return MCB_OK;
@@ -424,7 +473,9 @@ struct DevBuf {
   uint32_t* tile_fn = nullptr;
   TilePartial* part = nullptr;
   mcb_trial_stats* out = nullptr;
-  size_t cap_fns = 0, cap_tiles = 0, cap_part = 0, cap_out = 0;
+  uint32_t* code = nullptr;
+  double* consts = nullptr;
+  size_t cap_fns = 0, cap_tiles = 0, cap_part = 0, cap_out = 0, cap_code = 0, cap_consts = 0;
 
   template <class T>
   static cudaError_t grow(T*& p, size_t& cap, size_t need) {
@@ -437,8 +488,11 @@ struct DevBuf {
     if (e == cudaSuccess) cap = n;
     return e;
   }
-  cudaError_t reserve(size_t n_fns, size_t n_tiles, size_t n_out) {
+  cudaError_t reserve(size_t n_fns, size_t n_tiles, size_t n_out, size_t n_code = 0,
+                      size_t n_consts = 0) {
     cudaError_t e;
+    if ((e = grow(code, cap_code, n_code)) != cudaSuccess) return e;
+    if ((e = grow(consts, cap_consts, n_consts)) != cudaSuccess) return e;
     if ((e = grow(fns, cap_fns, n_fns)) != cudaSuccess) return e;
     if ((e = grow(tile_fn, cap_tiles, n_tiles)) != cudaSuccess) return e;
     if ((e = grow(part, cap_part, n_tiles)) != cudaSuccess) return e;
@@ -449,6 +503,8 @@ struct DevBuf {
     if (tile_fn) cudaFree(tile_fn);
     if (part) cudaFree(part);
     if (out) cudaFree(out);
+    if (code) cudaFree(code);
+    if (consts) cudaFree(consts);
     *this = DevBuf{};
   }
 };
@@ -462,12 +518,23 @@ mcb_status enqueue_run(const HostPlan& hp, DevBuf& buf, uint32_t trials, const F
   if (upload) {
     if ((e = cudaMemcpyAsync(buf.fns, staged, sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice, s)) != cudaSuccess)
       return cuda_fail(e, "cudaMemcpyAsync(descriptors)");
+    if (!hp.code.empty() &&
+        ((e = cudaMemcpyAsync(buf.code, hp.code.data(), sizeof(uint32_t) * hp.code.size(),
+                              cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+         (!hp.consts.empty() &&
+          (e = cudaMemcpyAsync(buf.consts, hp.consts.data(), sizeof(double) * hp.consts.size(),
+                               cudaMemcpyHostToDevice, s)) != cudaSuccess)))
+      return cuda_fail(e, "cudaMemcpyAsync(programs)");
     if ((e = mcb::detail::launch_expand_tiles(buf.fns, n_fns, trials, buf.tile_fn, s)) != cudaSuccess)
       return cuda_fail(e, "launch k_expand_tiles");
   }
-  for (const auto& g : hp.groups)
-    if ((e = mcb::detail::launch_direct_group(g, buf.fns, buf.tile_fn, buf.part, s)) != cudaSuccess)
-      return cuda_fail(e, "launch k_direct");
+  for (const auto& g : hp.groups) {
+    if (g.family == MCB_FAMILY_PROGRAM)
+      e = mcb::detail::launch_program_group(g, buf.fns, buf.tile_fn, buf.part, buf.code, buf.consts, s);
+    else
+      e = mcb::detail::launch_direct_group(g, buf.fns, buf.tile_fn, buf.part, s);
+    if (e != cudaSuccess) return cuda_fail(e, "launch k_direct");
+  }
   if ((e = mcb::detail::launch_combine(buf.fns, n_fns, trials, buf.part, buf.out, s)) != cudaSuccess)
     return cuda_fail(e, "launch k_combine");
   return MCB_OK;
@@ -523,7 +590,8 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
     c.ready = true;
   }
   const size_t n_out = n_fns * trials;
-  if ((e = c.buf.reserve(n_fns, hp.n_tiles, n_out)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  if ((e = c.buf.reserve(n_fns, hp.n_tiles, n_out, hp.code.size(), hp.consts.size())) != cudaSuccess)
+    return cuda_fail(e, "cudaMalloc");
   if ((e = grow_pinned(c.h_descs, c.h_descs_cap, n_fns)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
   if ((e = grow_pinned(c.h_out, c.h_out_cap, n_out)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
   std::memcpy(c.h_descs, hp.descs.data(), sizeof(FnDesc) * n_fns);
@@ -568,9 +636,16 @@ mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t see
     return st;
   }
   DeviceGuard guard(device);
-  cudaError_t e = plan->buf.reserve(n_fns, plan->hp.n_tiles, n_fns * trials);
+  cudaError_t e = plan->buf.reserve(n_fns, plan->hp.n_tiles, n_fns * trials, plan->hp.code.size(),
+                                    plan->hp.consts.size());
   if (e == cudaSuccess)
     e = cudaMemcpy(plan->buf.fns, plan->hp.descs.data(), sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !plan->hp.code.empty())
+    e = cudaMemcpy(plan->buf.code, plan->hp.code.data(), sizeof(uint32_t) * plan->hp.code.size(),
+                   cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !plan->hp.consts.empty())
+    e = cudaMemcpy(plan->buf.consts, plan->hp.consts.data(), sizeof(double) * plan->hp.consts.size(),
+                   cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = mcb::detail::launch_expand_tiles(plan->buf.fns, uint32_t(n_fns), trials, plan->buf.tile_fn, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -869,23 +944,49 @@ mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial
   if (st != MCB_OK) return st;
   if (count == 0) return MCB_OK;
   DeviceGuard guard(device);
-  const Prepared p = prepare(*fn, seed, 0, 0);
+  Prepared p = prepare(*fn, seed, 0, 0);
   const uint64_t first_pair = first_point / 2;
   const uint64_t n_pairs = (first_point + count - 1) / 2 - first_pair + 1;
+  const bool is_prog = fn->family == MCB_FAMILY_PROGRAM;
   FnDesc* d_fn = nullptr;
   double* d_out = nullptr;
+  uint32_t* d_code = nullptr;
+  double* d_consts = nullptr;
+  if (is_prog) {
+    p.d.prog_off = 0;
+    p.d.prog_len = uint32_t(fn->program->words.size());
+    p.d.const_off = 0;
+    p.d.n_consts = uint32_t(fn->program->p.consts.size());
+  }
   MCB_CUDA(cudaMalloc(&d_fn, sizeof(FnDesc)));
   cudaError_t e = cudaMalloc(&d_out, sizeof(double) * 2 * n_pairs);
   if (e == cudaSuccess) e = cudaMemcpy(d_fn, &p.d, sizeof(FnDesc), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess)
-    e = mcb::detail::launch_debug_eval_impl(int(fn->family), int(fn->dim), p.variant, d_fn, trial,
-                                            uint32_t(chunk), uint32_t(first_pair), uint32_t(n_pairs),
-                                            d_out, nullptr);
+  if (e == cudaSuccess && is_prog) {
+    const auto& w = fn->program->words;
+    const auto& c = fn->program->p.consts;
+    e = cudaMalloc(&d_code, sizeof(uint32_t) * std::max<size_t>(w.size(), 1));
+    if (e == cudaSuccess) e = cudaMalloc(&d_consts, sizeof(double) * std::max<size_t>(c.size(), 1));
+    if (e == cudaSuccess) e = cudaMemcpy(d_code, w.data(), sizeof(uint32_t) * w.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !c.empty())
+      e = cudaMemcpy(d_consts, c.data(), sizeof(double) * c.size(), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) {
+    if (is_prog)
+      e = mcb::detail::launch_program_eval(int(fn->dim), p.variant, d_fn, d_code, d_consts,
+                                           fn->program->p.depth, trial, uint32_t(chunk),
+                                           uint32_t(first_pair), uint32_t(n_pairs), d_out, nullptr);
+    else
+      e = mcb::detail::launch_debug_eval_impl(int(fn->family), int(fn->dim), p.variant, d_fn, trial,
+                                              uint32_t(chunk), uint32_t(first_pair),
+                                              uint32_t(n_pairs), d_out, nullptr);
+  }
   std::vector<double> tmp(2 * n_pairs);
   if (e == cudaSuccess)
     e = cudaMemcpy(tmp.data(), d_out, sizeof(double) * 2 * n_pairs, cudaMemcpyDeviceToHost);
   cudaFree(d_fn);
   if (d_out) cudaFree(d_out);
+  if (d_code) cudaFree(d_code);
+  if (d_consts) cudaFree(d_consts);
   if (e != cudaSuccess) return cuda_fail(e, "debug_eval");
   std::memcpy(out, tmp.data() + (first_point - 2 * first_pair), sizeof(double) * count);
   return MCB_OK;
@@ -924,6 +1025,60 @@ mcb_status mcb_probe_philox_peak(int device, double ms, double* blocks_per_s) {
   if (e != cudaSuccess) return cuda_fail(e, "philox_probe");
   *blocks_per_s = double(ctas) * 256.0 * 4.0 * double(iters) / (double(elapsed) * 1e-3);
   return MCB_OK;
+}
+
+mcb_status mcb_program_compile(const char* source, uint32_t dim, const char* const* param_names,
+                               size_t n_params, mcb_program** out) {
+  if (!source || !out || (n_params && !param_names))
+    return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  std::vector<std::string> names;
+  for (size_t i = 0; i < n_params; ++i) {
+    if (!param_names[i]) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL parameter name");
+    names.emplace_back(param_names[i]);
+  }
+  std::sort(names.begin(), names.end());
+  names.erase(std::unique(names.begin(), names.end()), names.end());
+  try {
+    auto* p = new mcb_program();
+    try {
+      p->p = mcb::prog::compile(source, dim, names);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    p->words = p->p.words();
+    *out = p;
+    return MCB_OK;
+  } catch (const mcb::prog::ParseError& e) {
+    return fail(MCB_ERR_VALIDATION, std::string("expression does not parse: ") + e.what());
+  } catch (const mcb::prog::CompileError& e) {
+    return fail(MCB_ERR_VALIDATION, e.what());
+  } catch (const std::exception& e) {
+    return fail(MCB_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+void mcb_program_destroy(mcb_program* program) { delete program; }
+
+mcb_status mcb_program_info(const mcb_program* program, uint32_t* n_instr, uint32_t* depth,
+                            uint32_t* n_params) {
+  if (!program) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL program");
+  if (n_instr) *n_instr = uint32_t(program->p.code.size());
+  if (depth) *depth = program->p.depth;
+  if (n_params) *n_params = uint32_t(program->p.param_names.size());
+  return MCB_OK;
+}
+
+size_t mcb_program_param_name(const mcb_program* program, uint32_t i, char* buf, size_t cap) {
+  if (!program || i >= program->p.param_names.size()) return 0;
+  const std::string& s = program->p.param_names[i];
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return s.size() + 1;
 }
 
 }  // extern "C"

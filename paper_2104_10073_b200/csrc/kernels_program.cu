@@ -1,0 +1,362 @@
+// kernels_program.cu — the direct-MC kernel for arbitrary DSL integrands
+// (MCB_FAMILY_PROGRAM): same sampler, tiles, reduction and combine as the
+// family kernels, with the integrand evaluated by a GPU interpreter of the
+// compiled postfix program (reference CompiledProgram::evaluate,
+// ref/src/expr.cpp:520-553).
+//
+// Interpreter layout (one CTA = one tile = one integrand, so the program is
+// uniform across the CTA and every switch is warp-uniform):
+//   * code words and constants staged in shared memory;
+//   * the evaluation stack as shared memory slots S[slot][h][tid] (h = the
+//     two samples of a pair, so every instruction is dispatched once for two
+//     samples), conflict-free because consecutive threads hit consecutive
+//     words;
+//   * the sample coordinates likewise, X[j][h][tid].
+// Every operation is the reference's: IEEE +,-,*,/ (correctly rounded, as
+// on the host), libdevice sin/cos/tan/asin/acos/atan/exp/log/pow (<= 2 ulp of
+// glibc), exact sqrt/fabs/floor/fmin/fmax.  Points are the same bit-exact
+// Philox stream; non-finite values are counted and skipped.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+#include <set>
+
+#include "kernels.cuh"
+#include "program.hpp"
+
+namespace mcb {
+namespace detail {
+
+constexpr int T = kProgThreads;
+
+__device__ __forceinline__ void interp_pair(const uint32_t* __restrict__ code, uint32_t len,
+                                            const double* __restrict__ consts,
+                                            const double* __restrict__ params, double* S,
+                                            const double* X) {
+  const int tid = threadIdx.x;
+  for (uint32_t pc = 0; pc < len; ++pc) {
+    const uint32_t w = code[pc];
+    const uint32_t op = w & 0xFFu, idx = w >> 20;
+    double* d = S + ((w >> 8) & 0xFu) * 2 * T + tid;
+    const double* a = S + ((w >> 12) & 0xFu) * 2 * T + tid;
+    const double* b = S + ((w >> 16) & 0xFu) * 2 * T + tid;
+#define MCB_UN(expr_)                          \
+  {                                            \
+    const double v0 = a[0], v1 = a[T];         \
+    d[0] = (expr_(0));                         \
+    d[T] = (expr_(1));                         \
+  }                                            \
+  break;
+#define MCB_BIN(expr_)                                           \
+  {                                                              \
+    const double v0 = a[0], v1 = a[T], w0 = b[0], w1 = b[T];     \
+    d[0] = (expr_(0));                                           \
+    d[T] = (expr_(1));                                           \
+  }                                                              \
+  break;
+    switch (op) {
+      case prog::kPushConst: {
+        const double c = consts[idx];
+        d[0] = c;
+        d[T] = c;
+      } break;
+      case prog::kLoadVar: {
+        const double* x = X + idx * 2 * T + tid;
+        d[0] = x[0];
+        d[T] = x[T];
+      } break;
+      case prog::kLoadParam: {
+        const double p = params[idx];
+        d[0] = p;
+        d[T] = p;
+      } break;
+#define NEG_(h) (-v##h)
+      case prog::kNeg: MCB_UN(NEG_)
+#define ADD_(h) __dadd_rn(v##h, w##h)
+      case prog::kAdd: MCB_BIN(ADD_)
+#define SUB_(h) __dsub_rn(v##h, w##h)
+      case prog::kSub: MCB_BIN(SUB_)
+#define MUL_(h) __dmul_rn(v##h, w##h)
+      case prog::kMul: MCB_BIN(MUL_)
+#define DIV_(h) __ddiv_rn(v##h, w##h)
+      case prog::kDiv: MCB_BIN(DIV_)
+#define POW_(h) pow(v##h, w##h)
+      case prog::kPow: MCB_BIN(POW_)
+#define SIN_(h) sin(v##h)
+      case prog::kSin: MCB_UN(SIN_)
+#define COS_(h) cos(v##h)
+      case prog::kCos: MCB_UN(COS_)
+#define TAN_(h) tan(v##h)
+      case prog::kTan: MCB_UN(TAN_)
+#define ASIN_(h) asin(v##h)
+      case prog::kAsin: MCB_UN(ASIN_)
+#define ACOS_(h) acos(v##h)
+      case prog::kAcos: MCB_UN(ACOS_)
+#define ATAN_(h) atan(v##h)
+      case prog::kAtan: MCB_UN(ATAN_)
+#define EXP_(h) exp(v##h)
+      case prog::kExp: MCB_UN(EXP_)
+#define LOG_(h) log(v##h)
+      case prog::kLog: MCB_UN(LOG_)
+#define SQRT_(h) __dsqrt_rn(v##h)
+      case prog::kSqrt: MCB_UN(SQRT_)
+#define ABS_(h) fabs(v##h)
+      case prog::kAbs: MCB_UN(ABS_)
+#define FLOOR_(h) floor(v##h)
+      case prog::kFloor: MCB_UN(FLOOR_)
+#define MIN_(h) fmin(v##h, w##h)
+      case prog::kMin: MCB_BIN(MIN_)
+#define MAX_(h) fmax(v##h, w##h)
+      case prog::kMax: MCB_BIN(MAX_)
+      default: {
+        d[0] = __longlong_as_double(0x7FF8000000000000ll);
+        d[T] = d[0];
+      }
+    }
+#undef MCB_UN
+#undef MCB_BIN
+  }
+}
+
+// Coordinates of the two samples of pair q into X[j][h][tid].
+template <int D, bool UNIT_DOM>
+__device__ __forceinline__ void gen_points(const FnDesc& f, const PhiloxPrefix& P, uint32_t q,
+                                           double* X) {
+  const uint64_t pbase = uint64_t(dev::kM0) * uint64_t(q * uint32_t(D));
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    uint32_t o[4];
+    dev::philox_block_p(P, pbase + uint64_t(i) * dev::kM0, o);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int t = 2 * i + hh, h = t / D, j = t % D;
+      const double u = __dmul_rn(hh ? dev::u_scaled(o[2], o[3]) : dev::u_scaled(o[0], o[1]),
+                                 dev::kTwoM64);
+      const double x = UNIT_DOM ? u : __dadd_rn(f.low[j], __dmul_rn(f.width[j], u));
+      X[(j * 2 + h) * T + threadIdx.x] = x;
+    }
+  }
+}
+
+// Shared memory: S[slots][2][T] | X[D][2][T] | consts[kMaxConsts] | code[kMaxCode]
+__host__ __device__ constexpr size_t program_smem_bytes(uint32_t slots, int dim) {
+  return (size_t(slots) + size_t(dim)) * 2 * T * sizeof(double) + prog::kMaxConsts * sizeof(double) +
+         prog::kMaxCode * sizeof(uint32_t);
+}
+
+struct ProgramSmem {
+  double* S;
+  double* X;
+  double* consts;
+  uint32_t* code;
+};
+
+template <int D>
+__device__ __forceinline__ ProgramSmem stage_program(const FnDesc& f, const uint32_t* __restrict__ code,
+                                                     const double* __restrict__ consts, uint32_t slots,
+                                                     double* params) {
+  extern __shared__ double dyn[];
+  ProgramSmem m;
+  m.S = dyn;
+  m.X = dyn + size_t(slots) * 2 * T;
+  m.consts = m.X + size_t(D) * 2 * T;
+  m.code = reinterpret_cast<uint32_t*>(m.consts + prog::kMaxConsts);
+  for (uint32_t i = threadIdx.x; i < f.prog_len; i += T) m.code[i] = code[f.prog_off + i];
+  for (uint32_t i = threadIdx.x; i < f.n_consts; i += T) m.consts[i] = consts[f.const_off + i];
+  if (threadIdx.x < prog::kMaxParams) params[threadIdx.x] = f.k[threadIdx.x];
+  __syncthreads();
+  return m;
+}
+
+template <int D, int V>
+__global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
+                                               const uint32_t* __restrict__ tile_fn, uint64_t tile0,
+                                               TilePartial* __restrict__ part,
+                                               const uint32_t* __restrict__ code,
+                                               const double* __restrict__ consts, uint32_t slots) {
+  constexpr bool UNIT_DOM = (V & kUnitDomain) != 0;
+  const uint64_t tile = tile0 + blockIdx.x;
+  const uint32_t fi = __ldg(tile_fn + tile);
+  const FnDesc f = fns[fi];
+  const uint32_t rem = uint32_t(tile - f.tile_base);
+  const uint32_t trial = rem / f.n_chunks;
+  const uint32_t chunk = rem - trial * f.n_chunks;
+  const uint32_t count =
+      (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
+                                : MCB_CHUNK_SIZE;
+  const uint32_t pairs = (count + 1) >> 1;
+  const PhiloxPrefix P =
+      dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
+  __shared__ double params[prog::kMaxParams];
+  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t nbad = 0;
+  for (uint32_t q = threadIdx.x; q < pairs; q += T) {
+    gen_points<D, UNIT_DOM>(f, P, q, m.X);
+    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+    const double f0 = m.S[threadIdx.x], f1 = m.S[T + threadIdx.x];
+    const bool has1 = 2 * q + 1 < count;
+    const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
+    nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+    const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
+    const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
+    s1 = __dadd_rn(s1, g0);
+    s2 = fma(g0, g0, s2);
+    s1 = __dadd_rn(s1, g1);
+    s2 = fma(g1, g1, s2);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    s1 = __dadd_rn(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, o));
+    s2 = __dadd_rn(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, o));
+    nbad += __shfl_xor_sync(0xFFFFFFFFu, nbad, o);
+  }
+  __shared__ double sh1[T / 32], sh2[T / 32];
+  __shared__ uint32_t shb[T / 32];
+  if ((threadIdx.x & 31) == 0) {
+    sh1[threadIdx.x >> 5] = s1;
+    sh2[threadIdx.x >> 5] = s2;
+    shb[threadIdx.x >> 5] = nbad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t1 = sh1[0], t2 = sh2[0];
+    uint32_t tb = shb[0];
+#pragma unroll
+    for (int w = 1; w < T / 32; ++w) {
+      t1 = __dadd_rn(t1, sh1[w]);
+      t2 = __dadd_rn(t2, sh2[w]);
+      tb += shb[w];
+    }
+    TilePartial p;
+    p.s1 = t1;
+    p.s2 = t2;
+    p.n_nonfinite = tb;
+    p.n_finite = count - tb;
+    part[tile] = p;
+  }
+}
+
+// Per-sample values of pairs [first_pair, first_pair + n_pairs) of one chunk
+// (test hook): exactly the gen_points/interp_pair of k_program.
+template <int D, int V>
+__global__ void __launch_bounds__(T) k_program_eval(const FnDesc* __restrict__ fn,
+                                                    const uint32_t* __restrict__ code,
+                                                    const double* __restrict__ consts, uint32_t slots,
+                                                    uint32_t trial, uint32_t chunk,
+                                                    uint32_t first_pair, uint32_t n_pairs,
+                                                    double* __restrict__ out) {
+  const FnDesc f = *fn;
+  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, chunk, trial);
+  __shared__ double params[prog::kMaxParams];
+  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  const uint32_t i = blockIdx.x * T + threadIdx.x;
+  gen_points<D, (V & kUnitDomain) != 0>(f, P, first_pair + i, m.X);
+  interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+  if (i < n_pairs) {
+    out[2 * uint64_t(i)] = m.S[threadIdx.x];
+    out[2 * uint64_t(i) + 1] = m.S[T + threadIdx.x];
+  }
+}
+
+// ---- dispatch ------------------------------------------------------------------
+
+using ProgFn = void (*)(const FnDesc*, const uint32_t*, uint64_t, TilePartial*, const uint32_t*,
+                        const double*, uint32_t);
+using ProgEvalFn = void (*)(const FnDesc*, const uint32_t*, const double*, uint32_t, uint32_t,
+                            uint32_t, uint32_t, uint32_t, double*);
+
+struct ProgEntry {
+  ProgFn run = nullptr;
+  ProgEvalFn eval = nullptr;
+};
+
+struct ProgTable {
+  ProgEntry e[MCB_MAX_DIM + 1][2];
+  template <int D>
+  void put() {
+    e[D][0] = {k_program<D, kSafe>, k_program_eval<D, kSafe>};
+    e[D][1] = {k_program<D, kSafe | kUnitDomain>, k_program_eval<D, kSafe | kUnitDomain>};
+  }
+  ProgTable() {
+    put<1>();
+    put<2>();
+    put<3>();
+    put<4>();
+    put<5>();
+    put<6>();
+    put<7>();
+    put<8>();
+  }
+};
+
+static const ProgTable& prog_table() {
+  static const ProgTable t;
+  return t;
+}
+
+// The >48 KB dynamic shared memory opt-in is per device: done once per
+// device on first use (the caller has the device current).
+static cudaError_t ensure_smem_optin() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(dev)) return cudaSuccess;
+  const ProgTable& t = prog_table();
+  for (int d = 1; d <= int(MCB_MAX_DIM); ++d)
+    for (int v = 0; v < 2; ++v) {
+      const int smem = int(program_smem_bytes(prog::kMaxDepth, d));
+      if ((e = cudaFuncSetAttribute(t.e[d][v].run, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem)) != cudaSuccess)
+        return e;
+      if ((e = cudaFuncSetAttribute(t.e[d][v].eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem)) != cudaSuccess)
+        return e;
+    }
+  done.insert(dev);
+  return cudaSuccess;
+}
+
+static const ProgEntry* prog_entry(int dim, int variant) {
+  if (dim < 1 || dim > int(MCB_MAX_DIM)) return nullptr;
+  return &prog_table().e[dim][(variant & kUnitDomain) ? 1 : 0];
+}
+
+cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const uint32_t* tile_fn,
+                                 TilePartial* part, const uint32_t* code, const double* consts,
+                                 cudaStream_t s) {
+  const ProgEntry* e = prog_entry(g.dim, g.variant);
+  if (!e) return cudaErrorInvalidValue;
+  if (cudaError_t err = ensure_smem_optin(); err != cudaSuccess) return err;
+  const size_t smem = program_smem_bytes(g.slots, g.dim);
+  const uint64_t kMaxGrid = 0x7FFFFFFFull;
+  for (uint64_t off = 0; off < g.n_tiles; off += kMaxGrid) {
+    const uint64_t n = g.n_tiles - off < kMaxGrid ? g.n_tiles - off : kMaxGrid;
+    e->run<<<dim3(uint32_t(n)), dim3(T), smem, s>>>(fns, tile_fn, g.tile0 + off, part, code, consts,
+                                                      g.slots);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_program_eval(int dim, int variant, const FnDesc* fn, const uint32_t* code,
+                                const double* consts, uint32_t slots, uint32_t trial, uint32_t chunk,
+                                uint32_t first_pair, uint32_t n_pairs, double* out, cudaStream_t s) {
+  const ProgEntry* e = prog_entry(dim, variant);
+  if (!e) return cudaErrorInvalidValue;
+  if (n_pairs == 0) return cudaSuccess;
+  if (cudaError_t err = ensure_smem_optin(); err != cudaSuccess) return err;
+  e->eval<<<(n_pairs + T - 1) / T, T, program_smem_bytes(slots, dim), s>>>(
+      fn, code, consts, slots, trial, chunk, first_pair, n_pairs, out);
+  return cudaGetLastError();
+}
+
+}  // namespace detail
+}  // namespace mcb

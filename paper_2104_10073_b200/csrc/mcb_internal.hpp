@@ -23,6 +23,7 @@ namespace detail {
 #define MCB_PIPELINE 1
 #endif
 constexpr int kThreads = MCB_THREADS;  // CTA size of the fused kernel
+constexpr int kProgThreads = 128;      // CTA size of the DSL-interpreter kernel
 
 enum Variant : int {
   kUnitDomain = 1,  // low == 0, width == 1 on every axis
@@ -39,6 +40,7 @@ enum Variant : int {
 struct GroupLaunch {
   int family, dim, variant;
   uint64_t tile0, n_tiles;
+  uint32_t slots = 0;  // PROGRAM family: max stack depth of the group's programs
 };
 
 bool variant_supported(int family, int dim, int variant);
@@ -58,6 +60,12 @@ cudaError_t launch_debug_points(uint32_t key0, uint32_t key1, uint32_t trial, ui
 cudaError_t launch_debug_eval_impl(int family, int dim, int variant, const dev::FnDesc* fn,
                                    uint32_t trial, uint32_t chunk, uint32_t first_pair,
                                    uint32_t n_pairs, double* out, cudaStream_t s);
+cudaError_t launch_program_group(const GroupLaunch& g, const dev::FnDesc* fns,
+                                 const uint32_t* tile_fn, dev::TilePartial* part,
+                                 const uint32_t* code, const double* consts, cudaStream_t s);
+cudaError_t launch_program_eval(int dim, int variant, const dev::FnDesc* fn, const uint32_t* code,
+                                const double* consts, uint32_t slots, uint32_t trial, uint32_t chunk,
+                                uint32_t first_pair, uint32_t n_pairs, double* out, cudaStream_t s);
 cudaError_t launch_philox_probe(const uint32_t* key, uint32_t* sink, int n_ctas, int iters,
                                cudaStream_t s);
 

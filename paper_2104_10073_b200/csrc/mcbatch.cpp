@@ -41,9 +41,24 @@ std::vector<std::string> required_params(const IntegrandSpec& s) {
     case Family::Abs2:
     case Family::Abs3:
       return {};  // "a" defaults to 1 ("abs(x1+x2)" has no parameter)
+    case Family::Program:
+      return {};  // bound at compile time (compile_program)
   }
   return {};
 }
+
+// Programs of one job, compiled once per distinct (source, dim, params).
+struct ProgramCache {
+  std::map<std::string, CompiledSource> by_key;
+  const mcb_program* get(const IntegrandSpec& s) {
+    std::string key = s.program_source + '\x1f' + std::to_string(s.dim);
+    for (const auto& [n, v] : s.params) key += '\x1f' + n;
+    auto it = by_key.find(key);
+    if (it == by_key.end())
+      it = by_key.emplace(key, compile_program(s.program_source, s.dim, s.params)).first;
+    return it->second.handle;
+  }
+};
 
 double param_or(const IntegrandSpec& s, const char* name, double dflt) {
   auto it = s.params.find(name);
@@ -98,7 +113,19 @@ std::vector<double> sample_uniform(const HyperRect& rect, const StreamKey& key, 
 
 const char* method_name(Method) { return "direct"; }
 
-mcb_integrand to_descriptor(const IntegrandSpec& s, std::uint32_t integrand_index) {
+CompiledSource compile_program(const std::string& source, std::size_t dim,
+                               const std::map<std::string, double>& params) {
+  std::vector<const char*> names;
+  for (const auto& [n, v] : params) names.push_back(n.c_str());
+  CompiledSource c;
+  const mcb_status st =
+      mcb_program_compile(source.c_str(), uint32_t(dim), names.data(), names.size(), &c.handle);
+  if (st != MCB_OK) throw std::invalid_argument(mcb_last_error());
+  return c;
+}
+
+mcb_integrand to_descriptor(const IntegrandSpec& s, std::uint32_t integrand_index,
+                            const mcb_program* program) {
   mcb_integrand d{};
   d.family = uint32_t(s.family);
   d.dim = uint32_t(s.dim);
@@ -121,6 +148,13 @@ mcb_integrand to_descriptor(const IntegrandSpec& s, std::uint32_t integrand_inde
     case Family::Abs3:
       d.a = param_or(s, "a", 1.0);
       break;
+    case Family::Program: {
+      std::size_t j = 0;
+      for (const auto& [n, v] : s.params)  // sorted, the binding order
+        if (j < MCB_MAX_PARAMS) d.k[j++] = v;
+      d.program = program;
+      break;
+    }
   }
   for (std::size_t j = 0; j < s.domain.dim() && j < MCB_MAX_DIM; ++j) {
     d.low[j] = s.domain.low[j];
@@ -130,6 +164,7 @@ mcb_integrand to_descriptor(const IntegrandSpec& s, std::uint32_t integrand_inde
 }
 
 std::string IntegrandSpec::source() const {
+  if (family == Family::Program) return program_source;
   mcb_integrand d = to_descriptor(*this, 0);
   std::string s(mcb_to_dsl(&d, nullptr, 0), '\0');
   mcb_to_dsl(&d, s.data(), s.size());
@@ -171,7 +206,9 @@ IntegrandSpec IntegrandSpec::from_source(std::string name, const std::string& so
       return s;
     }
   }
-  throw std::invalid_argument("source is not one of the built-in families: " + source);
+  s.family = Family::Program;  // any other source: the GPU interpreter
+  s.program_source = source;
+  return s;
 }
 
 // ---- validation (src/batch.cpp:62-120) --------------------------------------
@@ -193,8 +230,17 @@ std::vector<Violation> validate(const JobSpec& job) {
   std::vector<Violation> out;
   std::vector<mcb_integrand> descs;
   std::vector<const char*> names;
+  ProgramCache programs;
   for (std::size_t i = 0; i < job.integrands.size(); ++i) {
     const IntegrandSpec& s = job.integrands[i];
+    const mcb_program* prog = nullptr;
+    if (s.family == Family::Program) {
+      try {
+        prog = programs.get(s);
+      } catch (const std::invalid_argument& e) {
+        out.push_back({s.name, e.what()});
+      }
+    }
     if (s.dim >= 1 && s.domain.dim() != s.dim && s.domain.valid())
       out.push_back({s.name, "domain dimension " + std::to_string(s.domain.dim()) +
                                  " does not match dim=" + std::to_string(s.dim)});
@@ -202,7 +248,7 @@ std::vector<Violation> validate(const JobSpec& job) {
       out.push_back({s.name, "domain is invalid (need low[i] < high[i], finite, dim >= 1)"});
     for (const std::string& p : required_params(s))
       if (!s.params.count(p)) out.push_back({s.name, "unbound parameter '" + p + "'"});
-    descs.push_back(to_descriptor(s, uint32_t(i)));
+    descs.push_back(to_descriptor(s, uint32_t(i), prog));
     names.push_back(s.name.c_str());
   }
   std::vector<mcb_violation> v(descs.size() * 8 + 8);
@@ -213,6 +259,7 @@ std::vector<Violation> validate(const JobSpec& job) {
     std::string msg = v[i].message;
     // the domain check above already reported these with the reference wording
     if (msg.rfind("domain is invalid", 0) == 0) continue;
+    if (msg.rfind("program family needs", 0) == 0) continue;  // reported by compile_program
     out.push_back({who, msg});
   }
   return out;
@@ -237,7 +284,9 @@ McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const S
   if (n_samples < 2) throw std::invalid_argument("n_samples must be >= 2");
   if (spec.domain.dim() != spec.dim)
     throw std::invalid_argument("program/domain dimension mismatch");
-  mcb_integrand d = to_descriptor(spec, key_base.integrand_index);
+  ProgramCache programs;
+  const mcb_program* prog = spec.family == Family::Program ? programs.get(spec) : nullptr;
+  mcb_integrand d = to_descriptor(spec, key_base.integrand_index, prog);
   d.n_samples = n_samples;
   mcb_trial_stats st{};
   check(mcb_direct_mc(&d, key_base.global_seed, key_base.trial_index, key_base.chunk_index, device,
@@ -290,7 +339,11 @@ BatchResult run_batch(const JobSpec& job) {
   const std::size_t n = job.integrands.size();
   const std::uint32_t trials = job.trials;
   std::vector<mcb_integrand> descs(n);
-  for (std::size_t i = 0; i < n; ++i) descs[i] = to_descriptor(job.integrands[i], uint32_t(i));
+  ProgramCache programs;
+  for (std::size_t i = 0; i < n; ++i) {
+    const IntegrandSpec& s = job.integrands[i];
+    descs[i] = to_descriptor(s, uint32_t(i), s.family == Family::Program ? programs.get(s) : nullptr);
+  }
   std::vector<mcb_trial_stats> out(n * trials);
   double seconds = 0.0;
   const int* devs = job.devices.empty() ? nullptr : job.devices.data();

@@ -25,9 +25,8 @@ class ChunkAccum(ctypes.Structure):
 
 
 def build() -> str:
-    src = os.path.join(ORACLE_DIR, "mcb_oracle.c")
-    if (not os.path.exists(ORACLE_SO)) or os.path.getmtime(ORACLE_SO) < os.path.getmtime(src):
-        subprocess.run(["make", "-s", "-C", ORACLE_DIR, "all"], check=True)
+    # make tracks mcb_oracle.c and include/mcb/mcb.h (the shared struct layouts)
+    subprocess.run(["make", "-s", "-C", ORACLE_DIR, "all"], check=True)
     return ORACLE_SO
 
 
@@ -148,6 +147,10 @@ def load_ref():
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, P(dbl)]),
         "ref_harmonic_job": (i32, [u32, u64, P(dbl), P(u64), P(u32)]),
         "ref_harmonic_closed_form": (dbl, [dbl]),
+        "ref_eval_source": (i32, [ctypes.c_char_p, u32, P(ctypes.c_char_p), P(dbl), sz, ctypes.c_void_p, u64,
+                                  ctypes.c_void_p]),
+        "ref_direct_mc_source": (i32, [ctypes.c_char_p, u32, P(ctypes.c_char_p), P(dbl), sz, P(dbl), P(dbl),
+                                       u64, u64, u32, u32, u64, P(TrialStats)]),
         "ref_analytic_harmonic": (dbl, [u32]),
     }
     for name, (res, args) in sig.items():

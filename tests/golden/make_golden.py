@@ -146,9 +146,87 @@ def main():
     g["harmonic_job"] = {"k": [H(k) for k in ks], "seed": seed.value, "trials": trials.value,
                          "analytic": [H(ref.ref_analytic_harmonic(n)) for n in range(1, 101)]}
 
+    # 6. arbitrary DSL programs (the GPU interpreter's parity anchors)
+    g["programs"] = make_program_goldens(ref)
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(g, fh, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))
+
+
+PROGRAM_CASES = [
+    # (source, dim, params, low, high, n_samples, seed, index, trial, chunk_base)
+    ("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, {"k": 8.116902097686662}, [0] * 4, [1] * 4,
+     150_000, 20200814, 0, 0, 0),
+    ("exp(-50*(x1-0.5)^2)", 1, {}, [0], [1], 100_000, 11, 3, 2, 0),
+    ("sqrt(x1)*log(x2+1) + pow(x1, x2)", 2, {}, [0, 0], [1, 2], 70_001, 5, 1, 0, 4),
+    ("min(x1,x2) - max(x1, 0.3) + floor(3*x1) / (1 + abs(x2-x1))", 2, {}, [-1, 0], [1, 1.5],
+     66_000, 77, 9, 1, 0),
+    ("tan(x1) + atan(x2) + asin(x1) - acos(x2)", 2, {}, [0, 0], [0.9, 0.9], 50_000, 3, 2, 0, 0),
+    ("log(x1)", 1, {}, [-1], [1], 20_000, 9, 0, 0, 0),
+    ("sqrt(-1-x1)", 1, {}, [0], [1], 1_000, 9, 0, 0, 0),
+    ("a*x1^2 + b*sin(c*x2) + e - pi*x3", 3, {"a": 1.5, "b": -0.25, "c": 7.0}, [0, -1, 0],
+     [2, 1, 0.5], 90_000, 42, 5, 3, 2),
+    ("-x1^2 + 2^-x2 - -x3", 3, {}, [-1, -1, -1], [1, 1, 1], 40_000, 8, 0, 0, 0),
+    ("7", 2, {}, [0, 0], [2, 2], 1_000, 1, 0, 0, 0),
+    ("x1*x2*x3*x4*x5*x6*x7", 7, {}, [0] * 7, [1] * 7, 65_537, 6, 6, 6, 6),
+    ("1.5e-3*x1 + 2.E1*x2 + 3.25E+0/x3", 3, {}, [0, 0, 1], [1, 1, 2], 30_000, 2, 0, 1, 0),
+]
+
+
+def random_source(rng, dim, params, depth=0, max_depth=4):
+    """Random well-formed DSL source over safe-ish operators."""
+    roll = rng.integers(0, 100)
+    if depth >= max_depth or roll < 35:
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            return repr(float(np.round(rng.uniform(0, 4), 3)))
+        if kind == 1 or not params:
+            return f"x{rng.integers(1, dim + 1)}"
+        return params[rng.integers(0, len(params))]
+    if roll < 45:
+        return f"-({random_source(rng, dim, params, depth + 1, max_depth)})"
+    if roll < 75:
+        op = ["+", "-", "*", "/", "^"][rng.integers(0, 5)]
+        l = random_source(rng, dim, params, depth + 1, max_depth)
+        r = random_source(rng, dim, params, depth + 1, max_depth)
+        return f"({l}){op}({r})"
+    if rng.integers(0, 100) < 20:
+        fn = ["pow", "min", "max"][rng.integers(0, 3)]
+        return f"{fn}({random_source(rng, dim, params, depth + 1, max_depth)}, " \
+               f"{random_source(rng, dim, params, depth + 1, max_depth)})"
+    fn = ["sin", "cos", "tan", "atan", "exp", "log", "sqrt", "abs", "floor", "asin", "acos"][rng.integers(0, 11)]
+    return f"{fn}({random_source(rng, dim, params, depth + 1, max_depth)})"
+
+
+def make_program_goldens(ref):
+    rng = np.random.default_rng(2104)
+    cases = list(PROGRAM_CASES)
+    for i in range(16):
+        src = random_source(rng, 3, ["a", "b"])
+        cases.append((src, 3, {"a": float(rng.uniform(-2, 2)), "b": float(rng.uniform(0, 3))},
+                      [0, 0, 0], [1, 1, 1], 20_000, 1000 + i, i, i % 3, 0))
+    out = []
+    for src, dim, params, lo, hi, n, seed, index, trial, cb in cases:
+        names = sorted(params)
+        cn = (ctypes.c_char_p * max(1, len(names)))(*[x.encode() for x in names])
+        vals = (ctypes.c_double * max(1, len(names)))(*[params[x] for x in names])
+        lo_c = (ctypes.c_double * dim)(*lo)
+        hi_c = (ctypes.c_double * dim)(*hi)
+        pts = np.zeros(64 * dim)
+        assert ref.ref_sample_uniform(dim, lo_c, hi_c, seed, index, trial, cb, 64, pts.ctypes.data) == 0
+        v = np.zeros(64)
+        rc = ref.ref_eval_source(src.encode(), dim, cn, vals, len(names), pts.ctypes.data, 64, v.ctypes.data)
+        assert rc == 0, (src, ref.ref_last_error())
+        st = mcb.TrialStats()
+        rc = ref.ref_direct_mc_source(src.encode(), dim, cn, vals, len(names), lo_c, hi_c, n, seed, index,
+                                      trial, cb, ctypes.byref(st))
+        assert rc == 0, (src, ref.ref_last_error())
+        out.append({"source": src, "dim": dim, "params": {k: H(float(x)) for k, x in params.items()},
+                    "low": [H(float(x)) for x in lo], "high": [H(float(x)) for x in hi],
+                    "n_samples": n, "seed": seed, "index": index, "trial": trial, "chunk_base": cb,
+                    "values": [H(float(x)) for x in v], "estimate": stats_json(st)})
+    return out
 
 
 def _as_stats(row):

@@ -1,0 +1,231 @@
+"""Arbitrary DSL integrands (MCB_FAMILY_PROGRAM): the
+GPU postfix interpreter against the reference.
+
+CPU tests pin the pure-Python DSL oracle (tests/_dsl_oracle.py) bit-exactly to
+values and estimates produced by the reference itself (golden "programs"),
+and check the host compiler's contract (errors in the reference's wording,
+stack depth / instruction counts).  GPU tests compare the interpreter with
+the golden values and with the oracle.
+
+Tolerances: per-sample values |gpu - ref| <= 1e-12 * max(1, |ref|) with the
+same non-finite pattern (libdevice transcendentals are within 2 ulp of
+glibc); estimates 1e-9 relative (floor 1e-12 of the per-sample scale);
+n_samples / n_nonfinite identical."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from tests import _dsl_oracle as dsl
+from tests import _oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.json")
+
+
+def fx(h):
+    return float.fromhex(h)
+
+
+@pytest.fixture(scope="module")
+def progs():
+    with open(GOLDEN) as fh:
+        return json.load(fh)["programs"]
+
+
+def _case(c):
+    params = {k: fx(v) for k, v in c["params"].items()}
+    lo = [fx(x) for x in c["low"]]
+    hi = [fx(x) for x in c["high"]]
+    return params, lo, hi
+
+
+# ------------------------------------------------------------------ CPU
+
+def test_oracle_values_match_reference(progs, oracle):
+    for c in progs:
+        params, lo, hi = _case(c)
+        p = dsl.Program(c["source"], c["dim"], params)
+        pts = _oracle.sample_uniform(lo, hi, c["seed"], c["index"], c["trial"], c["chunk_base"], 0, 64)
+        got = np.array([p(row) for row in pts])
+        want = np.array([fx(v) for v in c["values"]])
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)) or \
+            np.allclose(got, want, rtol=0, atol=0, equal_nan=True), c["source"]
+
+
+def test_oracle_estimates_match_reference(progs, oracle):
+    for c in progs:
+        if c["n_samples"] > 100_000:
+            continue  # pure-Python Welford: keep the CPU suite fast
+        params, lo, hi = _case(c)
+        p = dsl.Program(c["source"], c["dim"], params)
+        n, chunks, rem = c["n_samples"], [], c["n_samples"]
+        ch = 0
+        while rem > 0:
+            cnt = min(65536, rem)
+            pts = _oracle.sample_uniform(lo, hi, c["seed"], c["index"], c["trial"], c["chunk_base"] + ch, 0, cnt)
+            chunks.append([p(row) for row in pts])
+            rem -= cnt
+            ch += 1
+        vol = 1.0
+        for a, b in zip(lo, hi):
+            vol *= b - a
+        res = dsl.welford_direct_mc(chunks, vol)
+        e = c["estimate"]
+        if e["status"] == 1:
+            assert res is None
+            continue
+        assert res[0] == fx(e["value"]) and res[1] == fx(e["std_error"]), c["source"]
+        assert (res[2], res[3]) == (e["n_samples"], e["n_nonfinite"])
+
+
+def test_compiler_contract(mcb):
+    p = mcb.Program("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, ["k"])
+    assert (p.n_instr, p.depth) == (21, 4)  # 21 instrs, stack 4
+    assert mcb.Program("a*x1 + b + c", 1, ["c", "a", "b"]).param_names == ["a", "b", "c"]
+    cases = {
+        "x3": "x3 exceeds dim=2",
+        "2+": "expression does not parse: expected a number, identifier or '(' (at offset 2)",
+        "q*x1": "unbound parameter 'q'",
+        "sin(x1,x2)": "function 'sin' expects 1 argument(s), got 2",
+        "foo(x1)": "unknown function 'foo'",
+        "sin": "expected '(' after function name 'sin'",
+        "1.5e": "unexpected trailing input",
+        "(x1": "expected ')'",
+        "x1 $ 2": "unexpected character '$'",
+        "": "empty expression",
+    }
+    for src, msg in cases.items():
+        with pytest.raises(mcb.McbError) as e:
+            mcb.Program(src, 2, ["a"])
+        assert e.value.status == 2 and msg in str(e.value), (src, str(e.value))
+    deep = "x1" + "+(x1" * 20 + ")" * 20
+    with pytest.raises(mcb.McbError) as e:
+        mcb.Program(deep, 1)
+    assert "stack slots" in str(e.value)
+
+
+def test_grammar_matches_oracle_parser(mcb):
+    """Precedence / associativity (ref tests/test_expr.cpp:30-42, 144-227):
+    the C++ compiler and the independent Python parser agree on values."""
+    rng = np.random.default_rng(424242)
+    ops = "+-*/^"
+    for _ in range(300):
+        src = ""
+        for t in range(int(rng.integers(1, 7))):
+            if t:
+                src += ops[int(rng.integers(0, 5))]
+            src += "-" * int(rng.integers(0, 3))
+            src += ["2", "3", "x1", "a", "0.5"][int(rng.integers(0, 5))]
+        p = dsl.Program(src, 1, {"a": 1.7})
+        q = mcb.Program(src, 1, ["a"])
+        assert q.n_instr == len(p.code), src
+    for src, val in [("2+3*4", 14.0), ("2^3^2", 512.0), ("-2^2", 4.0), ("2^-1", 0.5), ("8/4/2", 1.0),
+                     ("2-3-4", -5.0)]:
+        assert dsl.Program(src, 1, {})([0.0]) == val
+
+
+def test_validate_reports_program_errors(mcb):
+    p_ok = mcb.Program("x1*a", 1, ["a"])
+    f = p_ok.integrand({"a": 2.0}, n_samples=1000)
+    assert mcb.validate([f], 2) == []
+    g = mcb.make_integrand(mcb.FAMILY_PROGRAM, 1, n_samples=1000)
+    assert any("program family needs a compiled program" in m for _, m in mcb.validate([g], 2))
+    h = p_ok.integrand({"a": 2.0}, n_samples=1000)
+    h.dim = 2
+    h.low[1], h.high[1] = 0.0, 1.0
+    assert any("compiled for dim=1" in m for _, m in mcb.validate([h], 2))
+
+
+# ------------------------------------------------------------------ GPU
+
+def _values_close(got, want):
+    bad_g, bad_w = ~np.isfinite(got), ~np.isfinite(want)
+    assert np.array_equal(bad_g, bad_w)
+    g, w = got[~bad_w], want[~bad_w]
+    return np.all(np.abs(g - w) <= 1e-12 * np.maximum(1.0, np.abs(w)))
+
+
+@pytest.mark.gpu
+def test_interpreter_values_match_reference(gpu, progs):
+    for c in progs:
+        params, lo, hi = _case(c)
+        p = gpu.Program(c["source"], c["dim"], list(params))
+        f = p.integrand(params, low=lo, high=hi, n_samples=c["n_samples"], index=c["index"])
+        got = gpu.debug_eval(f, c["seed"], c["trial"], c["chunk_base"], 0, 64)
+        want = np.array([fx(v) for v in c["values"]])
+        assert _values_close(got, want), c["source"]
+        # odd offsets inside the chunk (pair straddling)
+        got2 = gpu.debug_eval(f, c["seed"], c["trial"], c["chunk_base"], 3, 61)
+        assert _values_close(got2, want[3:]), c["source"]
+
+
+@pytest.mark.gpu
+def test_interpreter_estimates_match_reference(gpu, progs):
+    for c in progs:
+        params, lo, hi = _case(c)
+        p = gpu.Program(c["source"], c["dim"], list(params))
+        f = p.integrand(params, low=lo, high=hi, n_samples=c["n_samples"], index=c["index"])
+        st = gpu.direct_mc(f, c["seed"], c["trial"], c["chunk_base"])
+        e = c["estimate"]
+        assert st.status == e["status"], c["source"]
+        assert (st.n_samples, st.n_nonfinite) == (e["n_samples"], e["n_nonfinite"]), c["source"]
+        if e["status"] != 0:
+            continue
+        vals = np.array([fx(v) for v in c["values"]])
+        fin = vals[np.isfinite(vals)]
+        scale = float(np.max(np.abs(fin))) if len(fin) else 1.0
+        vol = 1.0
+        for a, b in zip(lo, hi):
+            vol *= b - a
+        want = fx(e["value"])
+        assert abs(st.value - want) <= 1e-9 * max(abs(want), 1e-3 * scale * vol), (c["source"], st.value, want)
+        se = fx(e["std_error"])
+        assert abs(st.std_error - se) <= 1e-9 * se + 1e-300, (c["source"], st.std_error, se)
+
+
+@pytest.mark.gpu
+def test_program_matches_family_path(gpu):
+    """The same Fig.1 integrand through the interpreter and the fused family
+    kernel agree to 1e-12 per trial (different sincos implementations)."""
+    from paper_2104_10073_b200 import workloads
+    fam = workloads.c1(200_000)[0][:5]
+    p = gpu.Program("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, ["k"])
+    progs = [p.integrand({"k": f.k[0]}, n_samples=200_000, index=f.integrand_index) for f in fam]
+    a = gpu.run_direct(fam, 20200814, 3)
+    b = gpu.run_direct(progs, 20200814, 3)
+    assert np.array_equal(a["n_samples"], b["n_samples"])
+    assert np.all(np.abs(a["value"] - b["value"]) <= 1e-12)
+
+
+@pytest.mark.gpu
+def test_mixed_families_and_programs_device_invariant(gpu):
+    from paper_2104_10073_b200 import workloads
+    fns = list(workloads.c5(samples=70_000, n_fns=16)[0])
+    p1 = gpu.Program("exp(-a*((x1-0.5)^2+(x2-0.5)^2))", 2, ["a"])
+    p2 = gpu.Program("log(x1)*x2 + floor(4*x3)", 3)
+    for i, (p, par) in enumerate([(p1, {"a": 100.0}), (p2, {}), (p1, {"a": 3.0})]):
+        fns.append(p.integrand(par, low=[-1, 0, 0][:p.dim], high=[1, 1, 1][:p.dim], n_samples=90_000,
+                               index=16 + i))
+    runs = [gpu.run_direct(fns, 99, 3, devices=d) for d in ([0], [0, 0], [0, 0, 0])]
+    assert runs[0].tobytes() == runs[1].tobytes() == runs[2].tobytes()
+    # the log(x1) program on x1 in [-1, 1] has ~half non-finite samples
+    assert 0.4 < runs[0][17]["n_nonfinite"][0] / 90_000 < 0.6
+
+
+@pytest.mark.gpu
+def test_random_programs_vs_oracle(gpu, oracle):
+    from tests.golden.make_golden import random_source
+    rng = np.random.default_rng(7)
+    for i in range(12):
+        src = random_source(rng, 3, ["a", "b"])
+        params = {"a": float(rng.uniform(-2, 2)), "b": float(rng.uniform(0, 3))}
+        p = dsl.Program(src, 3, params)
+        q = gpu.Program(src, 3, list(params))
+        n = 3000
+        f = q.integrand(params, n_samples=n, index=i)
+        got = gpu.debug_eval(f, 555, 1, 2, 0, n)
+        pts = _oracle.sample_uniform([0.0] * 3, [1.0] * 3, 555, i, 1, 2, 0, n)
+        want = np.array([p(row) for row in pts])
+        assert _values_close(got, want), src
