@@ -443,7 +443,7 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
         hp.consts.insert(hp.consts.end(), pg->p.consts.begin(), pg->p.consts.end());
       }
       d.prog_off = it->second.first;
-      d.prog_len = uint32_t(pg->words.size());
+      d.prog_len = uint32_t(pg->p.code.size());
       d.const_off = it->second.second;
       d.n_consts = uint32_t(pg->p.consts.size());
       slots = pg->p.depth;
@@ -954,7 +954,7 @@ mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial
   double* d_consts = nullptr;
   if (is_prog) {
     p.d.prog_off = 0;
-    p.d.prog_len = uint32_t(fn->program->words.size());
+    p.d.prog_len = uint32_t(fn->program->p.code.size());
     p.d.const_off = 0;
     p.d.n_consts = uint32_t(fn->program->p.consts.size());
   }

@@ -31,92 +31,72 @@ namespace detail {
 
 constexpr int T = kProgThreads;
 
+// Operand fetch for the two samples (h = 0, 1): slots and variables live in
+// shared memory [index][h][tid]; constants and parameters are uniform.
+__device__ __forceinline__ void fetch(uint32_t kind, uint32_t idx, const double* S, const double* X,
+                                      const double* consts, const double* params, double& v0,
+                                      double& v1) {
+  if (kind <= prog::kVar) {
+    const double* p = (kind == prog::kSlot ? S : X) + idx * 2 * T + threadIdx.x;
+    v0 = p[0];
+    v1 = p[T];
+  } else {
+    v0 = v1 = (kind == prog::kConst ? consts[idx] : params[idx]);
+  }
+}
+
 __device__ __forceinline__ void interp_pair(const uint32_t* __restrict__ code, uint32_t len,
                                             const double* __restrict__ consts,
                                             const double* __restrict__ params, double* S,
                                             const double* X) {
   const int tid = threadIdx.x;
   for (uint32_t pc = 0; pc < len; ++pc) {
-    const uint32_t w = code[pc];
-    const uint32_t op = w & 0xFFu, idx = w >> 20;
-    double* d = S + ((w >> 8) & 0xFu) * 2 * T + tid;
-    const double* a = S + ((w >> 12) & 0xFu) * 2 * T + tid;
-    const double* b = S + ((w >> 16) & 0xFu) * 2 * T + tid;
-#define MCB_UN(expr_)                          \
-  {                                            \
-    const double v0 = a[0], v1 = a[T];         \
-    d[0] = (expr_(0));                         \
-    d[T] = (expr_(1));                         \
-  }                                            \
-  break;
-#define MCB_BIN(expr_)                                           \
-  {                                                              \
-    const double v0 = a[0], v1 = a[T], w0 = b[0], w1 = b[T];     \
-    d[0] = (expr_(0));                                           \
-    d[T] = (expr_(1));                                           \
-  }                                                              \
-  break;
+    const uint32_t w0 = code[2 * pc], w1 = code[2 * pc + 1];
+    const uint32_t op = w0 & 0xFFu;
+    double a0, a1, b0 = 0.0, b1 = 0.0, r0, r1;
+    fetch((w0 >> 18) & 3u, w1 & 0xFFFFu, S, X, consts, params, a0, a1);
     switch (op) {
-      case prog::kPushConst: {
-        const double c = consts[idx];
-        d[0] = c;
-        d[T] = c;
-      } break;
-      case prog::kLoadVar: {
-        const double* x = X + idx * 2 * T + tid;
-        d[0] = x[0];
-        d[T] = x[T];
-      } break;
-      case prog::kLoadParam: {
-        const double p = params[idx];
-        d[0] = p;
-        d[T] = p;
-      } break;
-#define NEG_(h) (-v##h)
-      case prog::kNeg: MCB_UN(NEG_)
-#define ADD_(h) __dadd_rn(v##h, w##h)
-      case prog::kAdd: MCB_BIN(ADD_)
-#define SUB_(h) __dsub_rn(v##h, w##h)
-      case prog::kSub: MCB_BIN(SUB_)
-#define MUL_(h) __dmul_rn(v##h, w##h)
-      case prog::kMul: MCB_BIN(MUL_)
-#define DIV_(h) __ddiv_rn(v##h, w##h)
-      case prog::kDiv: MCB_BIN(DIV_)
-#define POW_(h) pow(v##h, w##h)
-      case prog::kPow: MCB_BIN(POW_)
-#define SIN_(h) sin(v##h)
-      case prog::kSin: MCB_UN(SIN_)
-#define COS_(h) cos(v##h)
-      case prog::kCos: MCB_UN(COS_)
-#define TAN_(h) tan(v##h)
-      case prog::kTan: MCB_UN(TAN_)
-#define ASIN_(h) asin(v##h)
-      case prog::kAsin: MCB_UN(ASIN_)
-#define ACOS_(h) acos(v##h)
-      case prog::kAcos: MCB_UN(ACOS_)
-#define ATAN_(h) atan(v##h)
-      case prog::kAtan: MCB_UN(ATAN_)
-#define EXP_(h) exp(v##h)
-      case prog::kExp: MCB_UN(EXP_)
-#define LOG_(h) log(v##h)
-      case prog::kLog: MCB_UN(LOG_)
-#define SQRT_(h) __dsqrt_rn(v##h)
-      case prog::kSqrt: MCB_UN(SQRT_)
-#define ABS_(h) fabs(v##h)
-      case prog::kAbs: MCB_UN(ABS_)
-#define FLOOR_(h) floor(v##h)
-      case prog::kFloor: MCB_UN(FLOOR_)
-#define MIN_(h) fmin(v##h, w##h)
-      case prog::kMin: MCB_BIN(MIN_)
-#define MAX_(h) fmax(v##h, w##h)
-      case prog::kMax: MCB_BIN(MAX_)
-      default: {
-        d[0] = __longlong_as_double(0x7FF8000000000000ll);
-        d[T] = d[0];
-      }
+      case prog::kAdd: case prog::kSub: case prog::kMul: case prog::kDiv:
+      case prog::kPow: case prog::kMin: case prog::kMax:
+        fetch((w0 >> 20) & 3u, w1 >> 16, S, X, consts, params, b0, b1);
+        break;
+      default:
+        break;
     }
-#undef MCB_UN
-#undef MCB_BIN
+    switch (op) {
+      case prog::kCopy: r0 = a0; r1 = a1; break;
+      case prog::kSinCos: {
+        double c0, c1;
+        sincos(a0, &r0, &c0);
+        sincos(a1, &r1, &c1);
+        double* d2 = S + ((w0 >> 13) & 31u) * 2 * T + tid;
+        d2[0] = c0;
+        d2[T] = c1;
+      } break;
+      case prog::kNeg: r0 = -a0; r1 = -a1; break;
+      case prog::kAdd: r0 = __dadd_rn(a0, b0); r1 = __dadd_rn(a1, b1); break;
+      case prog::kSub: r0 = __dsub_rn(a0, b0); r1 = __dsub_rn(a1, b1); break;
+      case prog::kMul: r0 = __dmul_rn(a0, b0); r1 = __dmul_rn(a1, b1); break;
+      case prog::kDiv: r0 = __ddiv_rn(a0, b0); r1 = __ddiv_rn(a1, b1); break;
+      case prog::kPow: r0 = pow(a0, b0); r1 = pow(a1, b1); break;
+      case prog::kSin: r0 = sin(a0); r1 = sin(a1); break;
+      case prog::kCos: r0 = cos(a0); r1 = cos(a1); break;
+      case prog::kTan: r0 = tan(a0); r1 = tan(a1); break;
+      case prog::kAsin: r0 = asin(a0); r1 = asin(a1); break;
+      case prog::kAcos: r0 = acos(a0); r1 = acos(a1); break;
+      case prog::kAtan: r0 = atan(a0); r1 = atan(a1); break;
+      case prog::kExp: r0 = exp(a0); r1 = exp(a1); break;
+      case prog::kLog: r0 = log(a0); r1 = log(a1); break;
+      case prog::kSqrt: r0 = __dsqrt_rn(a0); r1 = __dsqrt_rn(a1); break;
+      case prog::kAbs: r0 = fabs(a0); r1 = fabs(a1); break;
+      case prog::kFloor: r0 = floor(a0); r1 = floor(a1); break;
+      case prog::kMin: r0 = fmin(a0, b0); r1 = fmin(a1, b1); break;
+      case prog::kMax: r0 = fmax(a0, b0); r1 = fmax(a1, b1); break;
+      default: r0 = r1 = __longlong_as_double(0x7FF8000000000000ll); break;
+    }
+    double* d = S + ((w0 >> 8) & 31u) * 2 * T + tid;
+    d[0] = r0;
+    d[T] = r1;
   }
 }
 
@@ -140,10 +120,10 @@ __device__ __forceinline__ void gen_points(const FnDesc& f, const PhiloxPrefix& 
   }
 }
 
-// Shared memory: S[slots][2][T] | X[D][2][T] | consts[kMaxConsts] | code[kMaxCode]
+// Shared memory: S[slots][2][T] | X[D][2][T] | consts[kMaxConsts] | code[2 * kMaxCode]
 __host__ __device__ constexpr size_t program_smem_bytes(uint32_t slots, int dim) {
   return (size_t(slots) + size_t(dim)) * 2 * T * sizeof(double) + prog::kMaxConsts * sizeof(double) +
-         prog::kMaxCode * sizeof(uint32_t);
+         2 * prog::kMaxCode * sizeof(uint32_t);
 }
 
 struct ProgramSmem {
@@ -163,7 +143,7 @@ __device__ __forceinline__ ProgramSmem stage_program(const FnDesc& f, const uint
   m.X = dyn + size_t(slots) * 2 * T;
   m.consts = m.X + size_t(D) * 2 * T;
   m.code = reinterpret_cast<uint32_t*>(m.consts + prog::kMaxConsts);
-  for (uint32_t i = threadIdx.x; i < f.prog_len; i += T) m.code[i] = code[f.prog_off + i];
+  for (uint32_t i = threadIdx.x; i < 2 * f.prog_len; i += T) m.code[i] = code[f.prog_off + i];
   for (uint32_t i = threadIdx.x; i < f.n_consts; i += T) m.consts[i] = consts[f.const_off + i];
   if (threadIdx.x < prog::kMaxParams) params[threadIdx.x] = f.k[threadIdx.x];
   __syncthreads();

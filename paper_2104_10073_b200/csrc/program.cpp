@@ -9,6 +9,7 @@
 #include <map>
 #include <memory>
 #include <numbers>
+#include <tuple>
 
 namespace mcb {
 namespace prog {
@@ -258,10 +259,20 @@ void collect(const Node& n, Symbols& out) {
   for (const auto& k : n.kids) collect(*k, out);
 }
 
-// Postfix emission with explicit slots: `sp` is the depth before the node.
-struct Emitter {
+// ---- DAG + slot allocation ----------------------------------------------------
+
+struct DagNode {
+  bool leaf = false;
+  Operand leaf_op;  // leaf: the operand
+  Op op = kAdd;     // internal: the operation
+  int a = -1, b = -1;
+};
+
+struct Lowering {
   Program& p;
-  std::map<uint64_t, uint32_t> const_index;  // bit pattern -> pool slot
+  std::vector<DagNode> nodes;
+  std::map<std::tuple<int, uint32_t, uint32_t, int, int>, int> index;  // hash-consing
+  std::map<uint64_t, uint32_t> const_index;
 
   uint32_t constant(double v) {
     uint64_t bits;
@@ -274,46 +285,143 @@ struct Emitter {
     return k;
   }
 
-  void push(Op op, uint32_t dst, uint32_t a, uint32_t b, uint32_t index) {
-    p.code.push_back(Instr{op, dst, a, b, index});
-    p.depth = std::max(p.depth, dst + 1);
+  int intern(const DagNode& n) {
+    const auto key = n.leaf ? std::make_tuple(-1, n.leaf_op.kind, n.leaf_op.index, -1, -1)
+                            : std::make_tuple(int(n.op), 0u, 0u, n.a, n.b);
+    auto it = index.find(key);
+    if (it != index.end()) return it->second;
+    nodes.push_back(n);
+    index.emplace(key, int(nodes.size() - 1));
+    return int(nodes.size() - 1);
   }
 
-  void emit(const Node& n, uint32_t sp) {
+  int leaf(uint32_t kind, uint32_t idx) {
+    DagNode n;
+    n.leaf = true;
+    n.leaf_op = Operand{kind, idx};
+    return intern(n);
+  }
+
+  // Tree -> DAG; counts the reference's postfix length on the way.
+  int lower(const Node& n) {
+    ++p.postfix_len;
     switch (n.kind) {
       case Node::Num:
-        push(kPushConst, sp, 0, 0, constant(n.value));
-        return;
+        return leaf(kConst, constant(n.value));
       case Node::Var:
         if (n.var >= p.dim)
           throw CompileError("x" + std::to_string(n.var + 1) + " exceeds dim=" + std::to_string(p.dim));
-        push(kLoadVar, sp, 0, 0, n.var);
-        return;
+        return leaf(kVar, n.var);
       case Node::Param: {
         auto it = std::find(p.param_names.begin(), p.param_names.end(), n.name);
         if (it == p.param_names.end()) throw CompileError("unbound parameter '" + n.name + "'");
-        push(kLoadParam, sp, 0, 0, uint32_t(it - p.param_names.begin()));
-        return;
+        return leaf(kParam, uint32_t(it - p.param_names.begin()));
       }
-      case Node::Neg:
-        emit(*n.kids[0], sp);
-        push(kNeg, sp, sp, 0, 0);
-        return;
+      case Node::Neg: {
+        DagNode d;
+        d.op = kNeg;
+        d.a = lower(*n.kids[0]);
+        return intern(d);
+      }
       case Node::Bin:
-      case Node::Call:
-        for (std::size_t i = 0; i < n.kids.size(); ++i) emit(*n.kids[i], sp + uint32_t(i));
-        push(n.op, sp, sp, sp + 1, 0);
-        return;
+      case Node::Call: {
+        DagNode d;
+        d.op = n.op;
+        d.a = lower(*n.kids[0]);
+        if (n.kids.size() > 1) d.b = lower(*n.kids[1]);
+        return intern(d);
+      }
     }
+    return -1;
+  }
+};
+
+struct Scheduler {
+  Program& p;
+  const std::vector<DagNode>& nodes;
+  std::vector<int> uses;       // remaining reads of each internal node
+  std::vector<int> slot;       // assigned slot (-1 = not yet computed)
+  std::vector<int> partner;    // sin <-> cos of the same argument
+  std::vector<bool> busy;      // slot occupancy
+  std::vector<int> need_;      // Sethi-Ullman register need (memoised)
+
+  // Slots a subtree needs when leaves are operands (0) and the child with
+  // the larger need is evaluated first; evaluation order does not change
+  // any value (every operation is a pure function of its operands).
+  int need(int id) {
+    const DagNode& n = nodes[size_t(id)];
+    if (n.leaf) return 0;
+    if (need_.empty()) need_.assign(nodes.size(), -1);
+    int& m = need_[size_t(id)];
+    if (m >= 0) return m;
+    const int a = need(n.a), b = n.b >= 0 ? need(n.b) : 0;
+    m = std::max(1, a == b ? a + (n.b >= 0 && b > 0 ? 1 : 0) : std::max(a, b));
+    return m;
+  }
+
+  uint32_t alloc() {
+    for (uint32_t s = 0; s < busy.size(); ++s)
+      if (!busy[s]) {
+        busy[s] = true;
+        p.depth = std::max(p.depth, s + 1);
+        return s;
+      }
+    busy.push_back(true);
+    p.depth = std::max(p.depth, uint32_t(busy.size()));
+    return uint32_t(busy.size() - 1);
+  }
+
+  Operand operand(int id) {
+    const DagNode& n = nodes[size_t(id)];
+    if (n.leaf) return n.leaf_op;
+    return Operand{kSlot, uint32_t(slot[size_t(id)])};
+  }
+
+  void release(int id) {
+    if (nodes[size_t(id)].leaf) return;
+    if (--uses[size_t(id)] == 0) busy[size_t(slot[size_t(id)])] = false;
+  }
+
+  void emit(int id) {
+    const DagNode& n = nodes[size_t(id)];
+    if (n.leaf || slot[size_t(id)] >= 0) return;
+    if (n.b >= 0 && need(n.b) > need(n.a)) {
+      emit(n.b);
+      emit(n.a);
+    } else {
+      emit(n.a);
+      if (n.b >= 0) emit(n.b);
+    }
+    Instr in;
+    in.op = n.op;
+    in.a = operand(n.a);
+    if (n.b >= 0) in.b = operand(n.b);
+    release(n.a);
+    if (n.b >= 0) release(n.b);
+    const int mate = partner[size_t(id)];
+    if (mate >= 0 && slot[size_t(mate)] < 0) {  // sin and cos of one argument: one sincos
+      const bool is_sin = n.op == kSin;
+      in.op = kSinCos;
+      const uint32_t s1 = alloc(), s2 = alloc();
+      slot[size_t(id)] = int(is_sin ? s1 : s2);
+      slot[size_t(mate)] = int(is_sin ? s2 : s1);
+      in.dst = s1;   // sin
+      in.dst2 = s2;  // cos
+      // the partner's read of the argument happens here too
+      release(n.a);
+    } else {
+      in.dst = alloc();
+      slot[size_t(id)] = int(in.dst);
+    }
+    p.code.push_back(in);
   }
 };
 
 }  // namespace
 
 std::vector<uint32_t> Program::words() const {
-  std::vector<uint32_t> w;
-  w.reserve(code.size());
-  for (const Instr& i : code) w.push_back(encode(i.op, i.dst, i.a, i.b, i.index));
+  std::vector<uint32_t> w(2 * code.size());
+  for (size_t i = 0; i < code.size(); ++i) encode(code[i], &w[2 * i]);
   return w;
 }
 
@@ -326,56 +434,104 @@ Symbols symbols(const std::string& source) {
 
 Program compile(const std::string& source, uint32_t dim,
                 const std::vector<std::string>& sorted_param_names) {
-  NodeP root = parse(source);
+  NodeP root_tree = parse(source);
   Program p;
   p.source = source;
   p.dim = dim;
   p.param_names = sorted_param_names;
-  Emitter em{p, {}};
-  em.emit(*root, 0);
-  if (p.depth > kMaxDepth)
-    throw CompileError("expression needs " + std::to_string(p.depth) +
-                       " stack slots; the GPU interpreter holds " + std::to_string(kMaxDepth));
-  if (p.code.size() > kMaxCode)
-    throw CompileError("expression compiles to " + std::to_string(p.code.size()) +
-                       " instructions; the GPU interpreter takes at most " +
-                       std::to_string(kMaxCode));
-  if (p.consts.size() > kMaxConsts) throw CompileError("too many distinct constants");
   if (p.param_names.size() > kMaxParams)
     throw CompileError("more than " + std::to_string(kMaxParams) + " parameters");
+  Lowering lw{p, {}, {}, {}};
+  const int root = lw.lower(*root_tree);
+  const auto& nodes = lw.nodes;
+  Scheduler sc{p, nodes, std::vector<int>(nodes.size(), 0), std::vector<int>(nodes.size(), -1),
+               std::vector<int>(nodes.size(), -1), {}};
+  // reads: one per operand position of every reachable internal node, plus the root
+  std::vector<bool> seen(nodes.size(), false);
+  std::vector<int> stack{root};
+  while (!stack.empty()) {
+    const int id = stack.back();
+    stack.pop_back();
+    if (seen[size_t(id)]) continue;
+    seen[size_t(id)] = true;
+    const DagNode& n = nodes[size_t(id)];
+    if (n.leaf) continue;
+    ++sc.uses[size_t(n.a)];
+    stack.push_back(n.a);
+    if (n.b >= 0) {
+      ++sc.uses[size_t(n.b)];
+      stack.push_back(n.b);
+    }
+  }
+  ++sc.uses[size_t(root)];
+  for (size_t i = 0; i < nodes.size(); ++i)
+    if (seen[i] && !nodes[i].leaf && (nodes[i].op == kSin || nodes[i].op == kCos))
+      for (size_t j = 0; j < nodes.size(); ++j)
+        if (j != i && seen[j] && !nodes[j].leaf && nodes[j].a == nodes[i].a &&
+            nodes[j].op == (nodes[i].op == kSin ? kCos : kSin))
+          sc.partner[i] = int(j);
+  sc.emit(root);
+  // the result must end in slot 0
+  const Operand r = sc.operand(root);
+  if (r.kind != kSlot || r.index != 0) {
+    Instr cp;
+    cp.op = kCopy;
+    cp.a = r;
+    cp.dst = 0;
+    p.depth = std::max(p.depth, 1u);
+    p.code.push_back(cp);
+  }
+  if (p.depth > kMaxDepth)
+    throw CompileError("expression needs " + std::to_string(p.depth) +
+                       " value slots; the GPU interpreter holds " + std::to_string(kMaxDepth));
+  if (p.code.size() > kMaxCode)
+    throw CompileError("expression compiles to " + std::to_string(p.code.size()) +
+                       " instructions; the GPU interpreter takes at most " + std::to_string(kMaxCode));
+  if (p.consts.size() > kMaxConsts) throw CompileError("too many distinct constants");
   return p;
 }
 
 double evaluate(const Program& p, const double* x, const double* params) {
   double st[kMaxDepth] = {};
-  for (const Instr& i : p.code) {
-    double& d = st[i.dst];
-    const double a = st[i.a], b = st[i.b];
-    switch (i.op) {
-      case kPushConst: d = p.consts[i.index]; break;
-      case kLoadVar: d = x[i.index]; break;
-      case kLoadParam: d = params[i.index]; break;
-      case kNeg: d = -a; break;
-      case kAdd: d = a + b; break;
-      case kSub: d = a - b; break;
-      case kMul: d = a * b; break;
-      case kDiv: d = a / b; break;
-      case kPow: d = std::pow(a, b); break;
-      case kSin: d = std::sin(a); break;
-      case kCos: d = std::cos(a); break;
-      case kTan: d = std::tan(a); break;
-      case kAsin: d = std::asin(a); break;
-      case kAcos: d = std::acos(a); break;
-      case kAtan: d = std::atan(a); break;
-      case kExp: d = std::exp(a); break;
-      case kLog: d = std::log(a); break;
-      case kSqrt: d = std::sqrt(a); break;
-      case kAbs: d = std::fabs(a); break;
-      case kFloor: d = std::floor(a); break;
-      case kMin: d = std::fmin(a, b); break;
-      case kMax: d = std::fmax(a, b); break;
-      default: d = NAN;
+  auto get = [&](const Operand& o) {
+    switch (o.kind) {
+      case kVar: return x[o.index];
+      case kConst: return p.consts[o.index];
+      case kParam: return params[o.index];
+      default: return st[o.index];
     }
+  };
+  for (const Instr& i : p.code) {
+    const double a = get(i.a), b = get(i.b);
+    double r = NAN;
+    switch (i.op) {
+      case kCopy: r = a; break;
+      case kSinCos:
+        st[i.dst2] = std::cos(a);
+        r = std::sin(a);
+        break;
+      case kNeg: r = -a; break;
+      case kAdd: r = a + b; break;
+      case kSub: r = a - b; break;
+      case kMul: r = a * b; break;
+      case kDiv: r = a / b; break;
+      case kPow: r = std::pow(a, b); break;
+      case kSin: r = std::sin(a); break;
+      case kCos: r = std::cos(a); break;
+      case kTan: r = std::tan(a); break;
+      case kAsin: r = std::asin(a); break;
+      case kAcos: r = std::acos(a); break;
+      case kAtan: r = std::atan(a); break;
+      case kExp: r = std::exp(a); break;
+      case kLog: r = std::log(a); break;
+      case kSqrt: r = std::sqrt(a); break;
+      case kAbs: r = std::fabs(a); break;
+      case kFloor: r = std::floor(a); break;
+      case kMin: r = std::fmin(a, b); break;
+      case kMax: r = std::fmax(a, b); break;
+      default: break;
+    }
+    st[i.dst] = r;
   }
   return st[0];
 }

@@ -13,8 +13,16 @@
 // (2 args); any other name is a free parameter.  Compilation emits postfix
 // in evaluation order (ref/src/expr.cpp:442-518): children left to right,
 // then the operator; parameters bind by position in the sorted name list
-// (ref/src/batch.cpp:129-140).  Each postfix instruction gets explicit
-// stack-slot operands so the device never tracks a stack pointer.
+// (ref/src/batch.cpp:129-140).
+//
+// For the GPU the tree is turned into a DAG (structurally identical pure
+// subexpressions computed once — exact, since every operation is a pure
+// function of its operands), sin/cos of the same argument fuse into one
+// sincos, leaves become operand modes (slot | variable | constant |
+// parameter) instead of load instructions, and values live in a small set
+// of register slots freed at their last use.  The Fig. 1 integrand
+// cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4)) is 21 postfix instructions in
+// the reference and 6 here.
 #pragma once
 
 #include <cstdint>
@@ -26,9 +34,8 @@ namespace mcb {
 namespace prog {
 
 enum Op : uint8_t {
-  kPushConst = 0,
-  kLoadVar,
-  kLoadParam,
+  kCopy = 0,  // dst = a
+  kSinCos,    // dst = sin(a), dst2 = cos(a)
   kNeg,
   kAdd,
   kSub,
@@ -51,21 +58,29 @@ enum Op : uint8_t {
   kNumOps
 };
 
-constexpr uint32_t kMaxDepth = 16;    // stack slots the GPU interpreter holds
-constexpr uint32_t kMaxCode = 1024;   // instructions per program
+constexpr uint32_t kMaxDepth = 16;    // value slots the GPU interpreter holds
+constexpr uint32_t kMaxCode = 1024;   // instructions per program (2 words each)
 constexpr uint32_t kMaxConsts = 512;  // constant-pool entries per program
 constexpr uint32_t kMaxParams = 8;    // parameter values carried per integrand
 
-// Device word: op (8) | dst slot (4) | a slot (4) | b slot (4) | index (12).
-inline uint32_t encode(Op op, uint32_t dst, uint32_t a, uint32_t b, uint32_t index) {
-  return uint32_t(op) | (dst << 8) | (a << 12) | (b << 16) | (index << 20);
-}
+enum OperandKind : uint32_t { kSlot = 0, kVar = 1, kConst = 2, kParam = 3 };
+struct Operand {
+  uint32_t kind = kSlot, index = 0;
+};
 
 struct Instr {
   Op op;
-  uint32_t dst, a, b;  // stack slots
-  uint32_t index;      // var / param / constant index
+  uint32_t dst = 0, dst2 = 0;  // result slot(s)
+  Operand a, b;
 };
+
+// Device encoding, two words per instruction:
+//   w0 = op (8) | dst (5) | dst2 (5) | a.kind (2) | b.kind (2)
+//   w1 = a.index (16) | b.index (16)
+inline void encode(const Instr& i, uint32_t w[2]) {
+  w[0] = uint32_t(i.op) | (i.dst << 8) | (i.dst2 << 13) | (i.a.kind << 18) | (i.b.kind << 20);
+  w[1] = (i.a.index & 0xFFFFu) | (i.b.index << 16);
+}
 
 struct ParseError : std::runtime_error {
   std::size_t offset;
@@ -83,8 +98,9 @@ struct Program {
   std::vector<std::string> param_names;  // sorted, as bound
   std::vector<Instr> code;
   std::vector<double> consts;
-  uint32_t depth = 0;                    // max stack depth
-  std::vector<uint32_t> words() const;   // device encoding
+  uint32_t depth = 0;                    // value slots used (result in slot 0)
+  uint32_t postfix_len = 0;              // the reference's postfix instruction count
+  std::vector<uint32_t> words() const;   // device encoding (2 words / instruction)
 };
 
 // Names of the free variables (0-based indices) and parameters (first
@@ -100,8 +116,8 @@ Symbols symbols(const std::string& source);
 Program compile(const std::string& source, uint32_t dim,
                 const std::vector<std::string>& sorted_param_names);
 
-// Reference-order scalar evaluation of a compiled program on the host (libm),
-// used for shift constants; the tests use the oracle instead.
+// Scalar evaluation of a compiled program on the host (libm), used for
+// shift constants; the tests use the oracle instead.
 double evaluate(const Program& p, const double* x, const double* params);
 
 }  // namespace prog

@@ -82,7 +82,11 @@ def test_oracle_estimates_match_reference(progs, oracle):
 
 def test_compiler_contract(mcb):
     p = mcb.Program("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, ["k"])
-    assert (p.n_instr, p.depth) == (21, 4)  # 21 instrs, stack 4
+    # reference postfix: 21 instructions, stack 4; the GPU
+    # form shares k*(x1+..+x4), fuses sin/cos into one sincos and folds loads
+    # into operands: Add, Add, Add, Mul, SinCos, Add in 3 slots
+    assert len(dsl.Program(p.source, 4, {"k": 1.0}).code) == 21
+    assert (p.n_instr, p.depth) == (6, 3)
     assert mcb.Program("a*x1 + b + c", 1, ["c", "a", "b"]).param_names == ["a", "b", "c"]
     cases = {
         "x3": "x3 exceeds dim=2",
@@ -100,10 +104,17 @@ def test_compiler_contract(mcb):
         with pytest.raises(mcb.McbError) as e:
             mcb.Program(src, 2, ["a"])
         assert e.value.status == 2 and msg in str(e.value), (src, str(e.value))
-    deep = "x1" + "+(x1" * 20 + ")" * 20
-    with pytest.raises(mcb.McbError) as e:
-        mcb.Program(deep, 1)
-    assert "stack slots" in str(e.value)
+    # deep right-nested expressions: the deeper operand is evaluated first
+    # (Sethi-Ullman), so a chain of 20 levels still needs 2 slots (the
+    # reference's stack machine needs 21)
+    deep = "".join(f"sin(x1*{i}+" for i in range(1, 21)) + "x1" + ")" * 20
+    assert mcb.Program(deep, 1).depth <= 2
+    wide = "+".join(f"sin({i}*x1)*cos({i}*x1)" for i in range(1, 30))
+    assert mcb.Program(wide, 1).depth <= 4
+    nested = "x1"
+    for i in range(1, 20):
+        nested = f"x1*(sin({i}*x1)+{nested})"
+    assert mcb.Program(nested, 1).depth <= 3
 
 
 def test_grammar_matches_oracle_parser(mcb):
@@ -120,7 +131,7 @@ def test_grammar_matches_oracle_parser(mcb):
             src += ["2", "3", "x1", "a", "0.5"][int(rng.integers(0, 5))]
         p = dsl.Program(src, 1, {"a": 1.7})
         q = mcb.Program(src, 1, ["a"])
-        assert q.n_instr == len(p.code), src
+        assert 1 <= q.n_instr <= len(p.code), src
     for src, val in [("2+3*4", 14.0), ("2^3^2", 512.0), ("-2^2", 4.0), ("2^-1", 0.5), ("8/4/2", 1.0),
                      ("2-3-4", -5.0)]:
         assert dsl.Program(src, 1, {})([0.0]) == val
