@@ -93,9 +93,23 @@ typedef struct mcb_integrand {
   double low[MCB_MAX_DIM];  /* HyperRect low  (include/mcbatch/sampling.hpp:14-24) */
   double high[MCB_MAX_DIM]; /* HyperRect high */
   const mcb_program* program; /* PROGRAM family only (not owned) */
+  uint32_t method;          /* mcb_method (reference Method, include/mcbatch/batch.hpp:18) */
+  uint32_t cells_per_dim;   /* STRATIFIED: k (0 = auto, ref src/batch.cpp:41-54) */
+  uint64_t cell_cap;        /* STRATIFIED: max k^d cells (0 = 1e6, RefineConfig::cell_cap) */
 } mcb_integrand;
 
-enum { MCB_TRIAL_OK = 0, MCB_TRIAL_ALL_NONFINITE = 1 };
+typedef enum mcb_method {
+  MCB_METHOD_DIRECT = 0,     /* direct_mc, ref src/estimator.cpp:75-92 */
+  MCB_METHOD_STRATIFIED = 1  /* k^d grid cells, direct_mc per cell, combine_cells
+                                (ref src/estimator.cpp:94-182, src/batch.cpp:255-275) */
+} mcb_method;
+
+enum {
+  MCB_TRIAL_OK = 0,
+  MCB_TRIAL_ALL_NONFINITE = 1, /* every sample non-finite (AllSamplesNonFinite) */
+  MCB_TRIAL_DEAD_CELL = 2      /* stratified: cell `detail` had no finite sample
+                                  (ref src/batch.cpp:176-180) */
+};
 
 /* Per-(integrand, trial) result = reference McEstimate
  * (include/mcbatch/estimator.hpp:18-25) plus a status replacing the
@@ -107,6 +121,8 @@ typedef struct mcb_trial_stats {
   uint64_t n_nonfinite;
   uint32_t status;    /* MCB_TRIAL_* */
   uint32_t nonfinite_warning;
+  uint32_t detail;    /* MCB_TRIAL_DEAD_CELL: index of the first dead cell */
+  uint32_t n_cells;   /* stratified: cells combined (1 for direct) */
 } mcb_trial_stats;
 
 /* One validation problem (reference Violation, include/mcbatch/batch.hpp:40-44).
@@ -136,6 +152,11 @@ MCB_API size_t mcb_to_dsl(const mcb_integrand* fn, char* buf, size_t cap);
  * duplicate-name check is skipped). Returns MCB_OK even if violations exist. */
 MCB_API mcb_status mcb_validate(const mcb_integrand* fns, size_t n_fns, const char* const* names,
                         uint32_t trials, mcb_violation* out, size_t cap, size_t* n_out);
+/* stratified_plan (ref src/batch.cpp:41-54): cells per dim, cells and
+ * samples per cell of a STRATIFIED integrand.  MCB_ERR_VALIDATION when the
+ * grid exceeds the cell cap ("cell grid exceeds configured cap"). */
+MCB_API mcb_status mcb_stratified_plan(const mcb_integrand* fn, uint32_t* cells_per_dim,
+                                       uint64_t* n_cells, uint32_t* samples_per_cell);
 /* LPT shard assignment of integrands to `n_shards` devices by estimated cost
  * n_samples * trials * per-sample cost(family, dim).  Deterministic. */
 MCB_API mcb_status mcb_partition(const mcb_integrand* fns, size_t n_fns, uint32_t trials,

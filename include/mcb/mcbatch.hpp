@@ -12,12 +12,14 @@
 //  * JobSpec::workers (CPU threads) becomes JobSpec::devices (CUDA ordinals).
 //    Results are byte-identical for any device list, the analogue of the
 //    reference's worker invariance (tests/test_batch.cpp:91-121).
-//  * Only Method::Direct exists (stratified/tree are out of scope).
+//  * Method::Direct and Method::Stratified run on the GPU; Method::Tree
+//    (sequential adaptive refinement) is not implemented.
 #pragma once
 
 #include <cstdint>
 #include <functional>
 #include <map>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -73,8 +75,19 @@ enum class Family {
   Program = MCB_FAMILY_PROGRAM            // any DSL source (`program_source`)
 };
 
-enum class Method { Direct };
+enum class Method { Direct, Stratified };
 const char* method_name(Method m);
+
+// include/mcbatch/estimator.hpp:39-46 (stratified uses init_cells_per_dim
+// and cell_cap; the tree fields are carried for source compatibility)
+struct RefineConfig {
+  std::uint32_t init_cells_per_dim = 0;  // 0 = auto (k^d <= min(4096, n/2))
+  std::uint32_t samples_per_cell = 2048;
+  std::uint32_t max_depth = 6;
+  double sigma_multiplier = 1.0;
+  std::uint64_t total_budget = 100000;
+  std::uint64_t cell_cap = 1000000;
+};
 
 // include/mcbatch/batch.hpp:22-31 with a family descriptor.
 struct IntegrandSpec {
@@ -86,6 +99,7 @@ struct IntegrandSpec {
   std::map<std::string, double> params;  // a, b, k | a, b, k1..kd | a
   std::uint64_t n_samples = 10000;
   Method method = Method::Direct;
+  std::optional<RefineConfig> method_config;
   std::string program_source;  // Family::Program: the DSL source
 
   // Exact reference DSL source of this descriptor.
@@ -161,6 +175,14 @@ struct BatchResult {
 
 // src/batch.cpp:195-333
 BatchResult run_batch(const JobSpec& job);
+
+// include/mcbatch/batch.hpp:84-91 (src/batch.cpp:41-54)
+struct StratifiedPlan {
+  std::uint32_t cells_per_dim = 1;
+  std::uint32_t samples_per_cell = 2;
+  std::uint64_t n_cells = 1;
+};
+StratifiedPlan stratified_plan(const IntegrandSpec& spec);
 
 // src/batch.cpp:335-367
 std::vector<TrialSummary> parameter_scan(const IntegrandSpec& tmpl, const std::string& param_name,

@@ -231,6 +231,7 @@ static void reduce_to_stats(double volume, const orc_chunk_accum* total, mcb_tri
   st->n_nonfinite = total->n_nonfinite;
   if (total->n == 0) { st->status = MCB_TRIAL_ALL_NONFINITE; return; }
   st->status = MCB_TRIAL_OK;
+  st->n_cells = 1;
   st->value = volume * total->mean;
   if (total->n >= 2) {
     double var = total->m2 / (double)(total->n - 1);
@@ -261,6 +262,108 @@ ORC_EXPORT int orc_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t tr
     orc_accum_merge(&total, &a);
   }
   reduce_to_stats(orc_volume(fn), &total, out);
+  return 0;
+}
+
+/* ---- stratified: src/batch.cpp:41-54, src/estimator.cpp:94-182 ---------- */
+
+/* cell_grid_size, src/estimator.cpp:94-105 (returns 0 past the cap) */
+static uint64_t cell_grid_size(uint32_t k, uint32_t d, uint64_t cap) {
+  if (k == 0) return 0;
+  uint64_t cells = 1;
+  for (uint32_t i = 0; i < d; ++i) {
+    if (cells > cap / k + 1) return 0;
+    cells *= k;
+  }
+  return cells > cap ? 0 : cells;
+}
+
+/* auto_cells_per_dim, src/estimator.cpp:107-122 */
+static uint32_t auto_cells_per_dim(uint32_t d, uint64_t limit) {
+  uint32_t k = 1;
+  for (;;) {
+    uint64_t cells = 1;
+    for (uint32_t i = 0; i < d; ++i) {
+      cells *= (uint64_t)k + 1;
+      if (cells > limit) return k;
+    }
+    ++k;
+  }
+}
+
+/* stratified_plan, src/batch.cpp:41-54 */
+ORC_EXPORT int orc_stratified_plan(const mcb_integrand* fn, uint32_t* k, uint64_t* n_cells,
+                                   uint32_t* spc) {
+  const uint64_t cap = fn->cell_cap ? fn->cell_cap : 1000000ull;
+  if (fn->cells_per_dim > 0) {
+    *k = fn->cells_per_dim;
+  } else {
+    uint64_t limit = fn->n_samples / 2 < 4096 ? fn->n_samples / 2 : 4096;
+    *k = auto_cells_per_dim(fn->dim, limit > 1 ? limit : 1);
+  }
+  *n_cells = cell_grid_size(*k, fn->dim, cap);
+  if (*n_cells == 0) return -1;
+  uint64_t per = fn->n_samples / *n_cells;
+  *spc = (uint32_t)(per > 2 ? per : 2);
+  return 0;
+}
+
+/* grid_cell, src/estimator.cpp:124-143 (axis 0 most significant) */
+ORC_EXPORT void orc_grid_cell(const mcb_integrand* fn, uint32_t k, uint64_t index, double* lo,
+                              double* hi) {
+  uint64_t rem = index;
+  for (int j = (int)fn->dim - 1; j >= 0; --j) {
+    uint32_t digit = (uint32_t)(rem % k);
+    rem /= k;
+    double width = fn->high[j] - fn->low[j];
+    lo[j] = digit == 0 ? fn->low[j] : fn->low[j] + width * ((double)digit / k);
+    hi[j] = digit + 1 == k ? fn->high[j] : fn->low[j] + width * ((double)(digit + 1) / k);
+  }
+}
+
+/* run_batch Stratified branch for one trial (src/batch.cpp:255-275 tasks,
+ * :172-186 assemble) = stratified_mc (src/estimator.cpp:161-182): direct_mc
+ * per cell with chunk keys c * chunks_per_cell, combine_cells
+ * (src/estimator.cpp:145-159).  status DEAD_CELL (detail = first dead cell)
+ * replaces "cell c produced no finite sample". */
+ORC_EXPORT int orc_stratified_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
+                                 uint64_t chunk_base, mcb_trial_stats* out) {
+  uint32_t k, spc;
+  uint64_t n_cells;
+  if (orc_stratified_plan(fn, &k, &n_cells, &spc) != 0) return -1;
+  const uint64_t cpc = orc_chunk_count(spc);
+  mcb_integrand cell = *fn;
+  cell.method = 0;
+  cell.n_samples = spc;
+  double value = 0.0, var = 0.0;
+  uint64_t n_all = 0, nn_all = 0;
+  int64_t dead = -1;
+  for (uint64_t c = 0; c < n_cells; ++c) {
+    orc_grid_cell(fn, k, c, cell.low, cell.high);
+    mcb_trial_stats st;
+    if (orc_direct_mc(&cell, seed, trial, chunk_base + c * cpc, &st) != 0) return -1;
+    n_all += st.n_samples;
+    nn_all += st.n_nonfinite;
+    if (st.status != MCB_TRIAL_OK) {
+      if (dead < 0) dead = (int64_t)c;
+      continue;
+    }
+    value += st.value;
+    var += st.std_error * st.std_error;
+  }
+  memset(out, 0, sizeof *out);
+  out->n_samples = n_all;
+  out->n_nonfinite = nn_all;
+  out->n_cells = (uint32_t)n_cells;
+  out->nonfinite_warning = (double)nn_all > MCB_NONFINITE_WARN_FRACTION * (double)n_all;
+  if (dead >= 0) {
+    out->status = MCB_TRIAL_DEAD_CELL;
+    out->detail = (uint32_t)dead;
+    return 0;
+  }
+  out->status = MCB_TRIAL_OK;
+  out->value = value;
+  out->std_error = sqrt(var);
   return 0;
 }
 
@@ -311,7 +414,10 @@ static void* orc_worker(void* arg) {
     if (u >= p->n_fns * p->trials) break;
     size_t i = u / p->trials;
     uint32_t t = (uint32_t)(u % p->trials);
-    if (orc_direct_mc(&p->fns[i], p->seed, t, 0, &p->out[u]) != 0) p->failed = 1;
+    int rc = p->fns[i].method == MCB_METHOD_STRATIFIED
+                 ? orc_stratified_mc(&p->fns[i], p->seed, t, 0, &p->out[u])
+                 : orc_direct_mc(&p->fns[i], p->seed, t, 0, &p->out[u]);
+    if (rc != 0) p->failed = 1;
   }
   return NULL;
 }

@@ -160,7 +160,13 @@ int ref_run_batch(const char* const* sources, const mcb_integrand* fns, std::siz
       s.domain = rect_of(fns[i].dim, fns[i].low, fns[i].high);
       s.params = params_of(fns[i]);
       s.n_samples = fns[i].n_samples;
-      s.method = Method::Direct;
+      s.method = fns[i].method == MCB_METHOD_STRATIFIED ? Method::Stratified : Method::Direct;
+      if (s.method == Method::Stratified) {
+        RefineConfig rc;
+        rc.init_cells_per_dim = fns[i].cells_per_dim;
+        if (fns[i].cell_cap) rc.cell_cap = fns[i].cell_cap;
+        s.method_config = rc;
+      }
       job.integrands.push_back(std::move(s));
     }
     BatchResult br = run_batch(job);

@@ -36,6 +36,10 @@ MAX_PARAMS = 8
 
 TRIAL_OK = 0
 TRIAL_ALL_NONFINITE = 1
+TRIAL_DEAD_CELL = 2
+
+METHOD_DIRECT = 0
+METHOD_STRATIFIED = 1
 
 STATUS = {0: "MCB_OK", 1: "MCB_ERR_INVALID_ARGUMENT", 2: "MCB_ERR_VALIDATION", 3: "MCB_ERR_CUDA",
           4: "MCB_ERR_NO_DEVICE", 5: "MCB_ERR_OUT_OF_RANGE", 6: "MCB_ERR_BUFFER_TOO_SMALL"}
@@ -53,14 +57,17 @@ class Integrand(ctypes.Structure):
                 ("integrand_index", ctypes.c_uint32), ("flags", ctypes.c_uint32),
                 ("n_samples", ctypes.c_uint64), ("a", ctypes.c_double), ("b", ctypes.c_double),
                 ("k", ctypes.c_double * MAX_DIM), ("low", ctypes.c_double * MAX_DIM),
-                ("high", ctypes.c_double * MAX_DIM), ("program", ctypes.c_void_p)]
+                ("high", ctypes.c_double * MAX_DIM), ("program", ctypes.c_void_p),
+                ("method", ctypes.c_uint32), ("cells_per_dim", ctypes.c_uint32),
+                ("cell_cap", ctypes.c_uint64)]
 
 
 class TrialStats(ctypes.Structure):
     """``mcb_trial_stats`` = reference McEstimate + status."""
     _fields_ = [("value", ctypes.c_double), ("std_error", ctypes.c_double),
                 ("n_samples", ctypes.c_uint64), ("n_nonfinite", ctypes.c_uint64),
-                ("status", ctypes.c_uint32), ("nonfinite_warning", ctypes.c_uint32)]
+                ("status", ctypes.c_uint32), ("nonfinite_warning", ctypes.c_uint32),
+                ("detail", ctypes.c_uint32), ("n_cells", ctypes.c_uint32)]
 
 
 class Violation(ctypes.Structure):
@@ -75,7 +82,8 @@ class PlanInfo(ctypes.Structure):
 
 
 TRIAL_DTYPE = np.dtype([("value", "<f8"), ("std_error", "<f8"), ("n_samples", "<u8"),
-                        ("n_nonfinite", "<u8"), ("status", "<u4"), ("nonfinite_warning", "<u4")])
+                        ("n_nonfinite", "<u8"), ("status", "<u4"), ("nonfinite_warning", "<u4"),
+                        ("detail", "<u4"), ("n_cells", "<u4")])
 assert TRIAL_DTYPE.itemsize == ctypes.sizeof(TrialStats)
 
 # Every symbol include/mcb/mcb.h declares (checked by tests/test_abi.py).
@@ -85,7 +93,7 @@ ABI_SYMBOLS = [
     "mcb_direct_mc", "mcb_plan_create", "mcb_plan_launch", "mcb_plan_download",
     "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
     "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
-    "mcb_program_param_name",
+    "mcb_program_param_name", "mcb_stratified_plan",
 ]
 
 
@@ -122,6 +130,7 @@ def _load() -> ctypes.CDLL:
         "mcb_program_destroy": (None, [vp]),
         "mcb_program_info": (i32, [vp, P(u32), P(u32), P(u32)]),
         "mcb_program_param_name": (sz, [vp, u32, ctypes.c_char_p, sz]),
+        "mcb_stratified_plan": (i32, [P(Integrand), P(u32), P(u64), P(u32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -254,6 +263,21 @@ def validate(fns: Sequence[Integrand], trials: int, names: Optional[Sequence[str
         cn = (ctypes.c_char_p * len(names))(*[s.encode() for s in names])
     _check(lib.mcb_validate(arr, len(arr), cn, trials, out, cap, ctypes.byref(n)))
     return [(int(out[i].integrand), out[i].message.decode()) for i in range(min(n.value, cap))]
+
+
+def stratify(f: Integrand, cells_per_dim: int = 0, cell_cap: int = 0) -> Integrand:
+    """Switch an integrand to the stratified method (ref src/estimator.cpp:161-182)."""
+    f.method = METHOD_STRATIFIED
+    f.cells_per_dim = cells_per_dim
+    f.cell_cap = cell_cap
+    return f
+
+
+def stratified_plan(f: Integrand):
+    """(cells_per_dim, n_cells, samples_per_cell) — ref src/batch.cpp:41-54."""
+    k, n, spc = ctypes.c_uint32(), ctypes.c_uint64(), ctypes.c_uint32()
+    _check(lib.mcb_stratified_plan(ctypes.byref(f), ctypes.byref(k), ctypes.byref(n), ctypes.byref(spc)))
+    return k.value, n.value, spc.value
 
 
 def partition(fns: Sequence[Integrand], trials: int, n_shards: int) -> np.ndarray:

@@ -68,6 +68,61 @@ uint64_t splitmix64(uint64_t z) {  // src/sampling.cpp:44-49
 
 uint64_t chunk_count(uint64_t n) { return (n + MCB_CHUNK_SIZE - 1) / MCB_CHUNK_SIZE; }
 
+// ---- stratified plan (ref src/batch.cpp:41-54, src/estimator.cpp:94-122) ----
+
+// cell_grid_size: k^d, failing past the cap (CellBudgetExceeded).
+bool cell_grid_size(uint32_t k, uint32_t d, uint64_t cap, uint64_t& cells) {
+  if (k == 0) return false;
+  cells = 1;
+  for (uint32_t i = 0; i < d; ++i) {
+    if (cells > cap / k + 1) return false;
+    cells *= k;
+  }
+  return cells <= cap;
+}
+
+// auto_cells_per_dim: the largest k with k^d <= limit (at least 1).
+uint32_t auto_cells_per_dim(uint32_t d, uint64_t limit) {
+  uint32_t k = 1;
+  for (;;) {
+    uint64_t cells = 1;
+    for (uint32_t i = 0; i < d; ++i) {
+      cells *= uint64_t(k) + 1;
+      if (cells > limit) return k;
+    }
+    ++k;
+  }
+}
+
+struct StratPlan {
+  uint32_t k = 1, spc = 2;
+  uint64_t n_cells = 1;
+  bool ok = false;
+};
+
+StratPlan stratified_plan(const mcb_integrand& f) {
+  StratPlan p;
+  const uint64_t cap = f.cell_cap ? f.cell_cap : 1000000ull;
+  if (f.cells_per_dim > 0) {
+    p.k = f.cells_per_dim;
+  } else {
+    const uint64_t limit = std::min<uint64_t>(4096, f.n_samples / 2);
+    p.k = auto_cells_per_dim(f.dim, std::max<uint64_t>(limit, 1));
+  }
+  p.ok = cell_grid_size(p.k, f.dim, cap, p.n_cells);
+  if (p.ok) p.spc = uint32_t(std::max<uint64_t>(2, f.n_samples / p.n_cells));  // as the reference
+  return p;
+}
+
+bool stratified(const mcb_integrand& f) { return f.method == MCB_METHOD_STRATIFIED; }
+
+// Samples one trial of an integrand really draws.
+uint64_t trial_samples(const mcb_integrand& f) {
+  if (!stratified(f)) return f.n_samples;
+  const StratPlan p = stratified_plan(f);
+  return p.n_cells * uint64_t(p.spc);
+}
+
 uint32_t min_dim(uint32_t family) {
   return family == MCB_FAMILY_ABS2 ? 2u : (family == MCB_FAMILY_ABS3 ? 3u : 1u);
 }
@@ -206,7 +261,20 @@ void violations_of(const mcb_integrand& f, uint32_t trials,
       !(f.family == MCB_FAMILY_HARMONIC && f.a == 1.0 && f.b == 1.0))
     out.push_back("unit-coefficient flag needs the harmonic family with a = b = 1");
   if (f.flags & ~MCB_FLAG_UNIT_COEFFS) out.push_back("unknown flag bits");
-  const uint64_t nc = chunk_count(f.n_samples);
+  if (f.method > MCB_METHOD_STRATIFIED) {
+    out.push_back("unknown method " + std::to_string(f.method));
+    return;
+  }
+  uint64_t nc = chunk_count(f.n_samples);
+  if (stratified(f) && f.dim >= 1 && f.dim <= MCB_MAX_DIM) {
+    const StratPlan sp = stratified_plan(f);
+    if (!sp.ok) {
+      out.push_back(f.cells_per_dim == 0 && f.cell_cap == 0 ? "cells_per_dim must be >= 1"
+                                                            : "cell grid exceeds configured cap");
+      return;
+    }
+    nc = sp.n_cells * chunk_count(sp.spc);
+  }
   if (nc > 0xFFFFFFFFull) out.push_back("samples exceed 2^32 chunks (chunk_index is 32-bit)");
   else if (nc * uint64_t(std::max(trials, 1u)) > 0xFFFFFFFFull)
     out.push_back("chunks x trials exceeds 2^32 work units for one integrand");
@@ -240,6 +308,18 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   d.key0 = key[0];
   d.key1 = key[1];
   d.n_chunks = uint32_t(chunk_count(f.n_samples));
+  d.dim = f.dim;
+  const bool strat = stratified(f);
+  double cell_k = 1.0;
+  if (strat) {  // tiles per trial = cells x chunks per cell
+    const StratPlan sp = stratified_plan(f);
+    d.strat_k = sp.k;
+    d.n_cells = uint32_t(sp.n_cells);
+    d.spc = sp.spc;
+    d.cpc = uint32_t(chunk_count(sp.spc));
+    d.n_chunks = d.n_cells * d.cpc;
+    cell_k = double(sp.k);
+  }
   d.chunk_base = chunk_base;
   d.trial_base = trial_base;
   d.n_samples = f.n_samples;
@@ -251,9 +331,10 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   bool finite = std::isfinite(f.a) && std::isfinite(f.b);
   for (uint32_t j = 0; j < f.dim; ++j) {
     d.low[j] = f.low[j];
+    d.high[j] = f.high[j];
     d.width[j] = f.high[j] - f.low[j];
     d.k[j] = f.k[j];
-    if (!(f.low[j] == 0.0 && f.high[j] == 1.0)) unit_dom = false;
+    if (strat || !(f.low[j] == 0.0 && f.high[j] == 1.0)) unit_dom = false;
     const double m = std::max(std::fabs(f.low[j]), std::fabs(f.high[j]));
     if (f.family == MCB_FAMILY_HARMONIC_VEC) {
       finite = finite && std::isfinite(f.k[j]);
@@ -267,7 +348,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   if (f.family == MCB_FAMILY_PROGRAM) {
     // interpreter: plain parameters, unscaled draws, non-finite counting
     for (uint32_t j = 0; j < MCB_MAX_DIM; ++j) d.k[j] = f.k[j];
-    p.variant = kSafe | (unit_dom ? kUnitDomain : 0);
+    p.variant = kSafe | (unit_dom ? kUnitDomain : 0) | (strat ? kStrat : 0);
     double mid[MCB_MAX_DIM];
     for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
     const double c = host_eval(f, mid);
@@ -291,7 +372,8 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
         for (uint32_t j = 0; j < f.dim; ++j) fast = fast && foldable(f.k[j]);
       else fast = foldable(f.a);
     } else {
-      for (uint32_t j = 0; j < f.dim; ++j) fast = fast && foldable(d.width[j]);
+      // cells are >= width/k wide (the device folds each cell's width)
+      for (uint32_t j = 0; j < f.dim; ++j) fast = fast && foldable(0.5 * d.width[j] / cell_k);
     }
   }
   if (fast) {
@@ -300,7 +382,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
       else if (f.family == MCB_FAMILY_HARMONIC_VEC)
         for (uint32_t j = 0; j < f.dim; ++j) d.k[j] = f.k[j] * kTwoM64;
       else d.a = f.a * kTwoM64;
-    } else {
+    } else if (!strat) {
       for (uint32_t j = 0; j < f.dim; ++j) d.width[j] = d.width[j] * kTwoM64;
     }
     p.variant = (unit_dom ? kUnitDomain : 0) | (unit_coef ? kUnitCoef : 0);
@@ -309,15 +391,16 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
     // cancel; a (near-)constant integrand keeps the shift (exact 0 variance).
     if (harm) {
       double sweep = 0.0;
-      for (uint32_t j = 0; j < f.dim; ++j)
+      for (uint32_t j = 0; j < f.dim; ++j)  // over one cell when stratified
         sweep += std::fabs(f.family == MCB_FAMILY_HARMONIC ? f.k[0] : f.k[j]) *
-                 (f.high[j] - f.low[j]);
+                 (f.high[j] - f.low[j]) / cell_k;
       if (sweep >= 0.05 && std::fabs(f.a) + std::fabs(f.b) > 0.0) p.variant |= kNoShift;
     }
   } else {
     p.variant = kSafe;
   }
   if (!harm) p.variant &= ~kUnitCoef;
+  if (strat) p.variant |= kStrat;
   // shift constant: f at the domain midpoint (reference op order, libm)
   double mid[MCB_MAX_DIM];
   for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
@@ -455,9 +538,15 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
     tile += nt;
     hp.descs[r] = d;
-    hp.total_samples += fns[i].n_samples * trials;
-    const uint64_t full = fns[i].n_samples / MCB_CHUNK_SIZE, last = fns[i].n_samples % MCB_CHUNK_SIZE;
-    const uint64_t pairs = full * (MCB_CHUNK_SIZE / 2) + (last + 1) / 2;
+    hp.total_samples += trial_samples(fns[i]) * trials;
+    uint64_t pairs;
+    if (d.strat_k > 0) {
+      const uint64_t full = d.spc / MCB_CHUNK_SIZE, last = d.spc % MCB_CHUNK_SIZE;
+      pairs = (full * (MCB_CHUNK_SIZE / 2) + (last + 1) / 2) * d.n_cells;
+    } else {
+      const uint64_t full = fns[i].n_samples / MCB_CHUNK_SIZE, last = fns[i].n_samples % MCB_CHUNK_SIZE;
+      pairs = full * (MCB_CHUNK_SIZE / 2) + (last + 1) / 2;
+    }
     hp.philox_blocks += pairs * blocks_per_pair(fns[i].family, fns[i].dim) * trials;
   }
   for (const auto& g : hp.groups)
@@ -676,7 +765,7 @@ void lpt(const mcb_integrand* fns, size_t n, uint32_t trials, int shards, uint32
   std::iota(order.begin(), order.end(), size_t(0));
   std::vector<double> cost(n);
   for (size_t i = 0; i < n; ++i)
-    cost[i] = double(fns[i].n_samples) * double(trials) * sample_cost(fns[i]);
+    cost[i] = double(trial_samples(fns[i])) * double(trials) * sample_cost(fns[i]);
   std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
   std::vector<double> load(size_t(shards), 0.0);
   for (size_t i : order) {
@@ -753,6 +842,18 @@ mcb_status mcb_validate(const mcb_integrand* fns, size_t n_fns, const char* cons
     out[i].integrand = v[i].first;
     std::snprintf(out[i].message, sizeof out[i].message, "%s", v[i].second.c_str());
   }
+  return MCB_OK;
+}
+
+mcb_status mcb_stratified_plan(const mcb_integrand* fn, uint32_t* cells_per_dim, uint64_t* n_cells,
+                               uint32_t* samples_per_cell) {
+  if (!fn) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL integrand");
+  if (fn->dim < 1 || fn->dim > MCB_MAX_DIM) return fail(MCB_ERR_INVALID_ARGUMENT, "bad dim");
+  const StratPlan p = stratified_plan(*fn);
+  if (!p.ok) return fail(MCB_ERR_VALIDATION, "cell grid exceeds configured cap");
+  if (cells_per_dim) *cells_per_dim = p.k;
+  if (n_cells) *n_cells = p.n_cells;
+  if (samples_per_cell) *samples_per_cell = p.spc;
   return MCB_OK;
 }
 
@@ -944,7 +1045,9 @@ mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial
   if (st != MCB_OK) return st;
   if (count == 0) return MCB_OK;
   DeviceGuard guard(device);
-  Prepared p = prepare(*fn, seed, 0, 0);
+  mcb_integrand direct = *fn;  // per-sample values on the integrand's own domain
+  direct.method = MCB_METHOD_DIRECT;
+  Prepared p = prepare(direct, seed, 0, 0);
   const uint64_t first_pair = first_point / 2;
   const uint64_t n_pairs = (first_point + count - 1) / 2 - first_pair + 1;
   const bool is_prog = fn->family == MCB_FAMILY_PROGRAM;

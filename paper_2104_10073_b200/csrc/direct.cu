@@ -31,8 +31,60 @@ __global__ void k_expand_tiles(const FnDesc* __restrict__ fns, uint32_t n_fns, u
   for (uint64_t t = threadIdx.x & 31; t < n; t += 32) tile_fn[base + t] = fi;
 }
 
+// Cell volume of stratified cell `cell` (runtime dim; same arithmetic as
+// dev::grid_cell / the reference's grid_cell + HyperRect::volume).
+__device__ double cell_volume(const FnDesc& F, uint32_t cell) {
+  double w[MCB_MAX_DIM];
+  uint32_t rem = cell;
+  const uint32_t k = F.strat_k;
+  for (int j = int(F.dim) - 1; j >= 0; --j) {
+    const uint32_t digit = rem % k;
+    rem /= k;
+    const double lo = F.low[j], wd = F.width[j];
+    const double cl = digit == 0 ? lo : __dadd_rn(lo, __dmul_rn(wd, __ddiv_rn(double(digit), double(k))));
+    const double ch = digit + 1 == k ? F.high[j]
+                                     : __dadd_rn(lo, __dmul_rn(wd, __ddiv_rn(double(digit + 1), double(k))));
+    w[j] = __dsub_rn(ch, cl);
+  }
+  double v = 1.0;
+  for (uint32_t j = 0; j < F.dim; ++j) v = __dmul_rn(v, w[j]);
+  return v;
+}
+
+struct Accum {  // ChunkAccum (ref src/estimator.cpp:9-34): n, n_nonfinite, mean, m2
+  uint64_t n = 0, nn = 0;
+  double mean = 0.0, m2 = 0.0;
+};
+
+// ChunkAccum::merge (ref src/estimator.cpp:20-34) of one tile whose partial
+// sums are taken about its own shift.
+__device__ __forceinline__ void merge_tile(Accum& a, const TilePartial& p) {
+  a.nn += p.n_nonfinite;
+  if (p.n_finite == 0) return;
+  const double n_b = double(p.n_finite);
+  const double dev_b = __ddiv_rn(p.s1, n_b);
+  const double mean_b = __dadd_rn(p.shift, dev_b);
+  double m2_b = __dsub_rn(p.s2, __dmul_rn(p.s1, dev_b));
+  m2_b = m2_b > 0.0 ? m2_b : 0.0;
+  if (a.n == 0) {
+    a.n = p.n_finite;
+    a.mean = mean_b;
+    a.m2 = m2_b;
+    return;
+  }
+  const double delta = __dsub_rn(mean_b, a.mean);
+  const uint64_t total = a.n + p.n_finite;
+  a.mean = __dadd_rn(a.mean, __dmul_rn(delta, __ddiv_rn(n_b, double(total))));
+  a.m2 = __dadd_rn(a.m2, __dadd_rn(m2_b, __dmul_rn(__dmul_rn(delta, delta),
+                                                    __ddiv_rn(__dmul_rn(double(a.n), n_b), double(total)))));
+  a.n = total;
+}
+
 // K4: ascending-chunk combine per (integrand, trial) and McEstimate fields
-// (reduce_chunks, src/estimator.cpp:55-73).
+// (reduce_chunks, src/estimator.cpp:55-73).  Stratified integrands: each
+// cell's chunks merge into the cell estimate, cells combine in ascending
+// order (combine_cells, src/estimator.cpp:145-159); a cell without finite
+// samples fails the trial (src/batch.cpp:176-180).
 __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32_t trials,
                           const TilePartial* __restrict__ part, mcb_trial_stats* __restrict__ out) {
   const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -40,6 +92,46 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
   const uint32_t fi = uint32_t(idx / trials), t = uint32_t(idx % trials);
   const FnDesc& F = fns[fi];
   const uint64_t base = F.tile_base + uint64_t(t) * F.n_chunks;
+  mcb_trial_stats st;
+  st.detail = 0;
+  st.n_cells = 1;
+  if (F.strat_k > 0) {
+    double value = 0.0, var = 0.0;
+    uint64_t n_all = 0, nn_all = 0;
+    int dead = -1;
+    for (uint32_t c = 0; c < F.n_cells; ++c) {
+      Accum a;
+      for (uint32_t cc = 0; cc < F.cpc; ++cc) merge_tile(a, part[base + uint64_t(c) * F.cpc + cc]);
+      n_all += a.n + a.nn;
+      nn_all += a.nn;
+      if (a.n == 0) {
+        if (dead < 0) dead = int(c);
+        continue;
+      }
+      const double vol = cell_volume(F, c);
+      value = __dadd_rn(value, __dmul_rn(vol, a.mean));
+      const double se = a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)),
+                                                                         double(a.n))))
+                                 : __longlong_as_double(0x7FF0000000000000ll);
+      var = __dadd_rn(var, __dmul_rn(se, se));
+    }
+    st.n_cells = F.n_cells;
+    st.n_samples = n_all;
+    st.n_nonfinite = nn_all;
+    st.nonfinite_warning = double(nn_all) > MCB_NONFINITE_WARN_FRACTION * double(n_all) ? 1u : 0u;
+    if (dead >= 0) {
+      st.status = MCB_TRIAL_DEAD_CELL;
+      st.detail = uint32_t(dead);
+      st.value = 0.0;
+      st.std_error = 0.0;
+    } else {
+      st.status = MCB_TRIAL_OK;
+      st.value = value;
+      st.std_error = __dsqrt_rn(var);
+    }
+    out[F.out_slot * trials + t] = st;
+    return;
+  }
   double s1 = 0.0, s2 = 0.0;
   uint64_t n = 0, nb = 0;
   for (uint32_t c = 0; c < F.n_chunks; ++c) {
@@ -49,7 +141,6 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
     n += p.n_finite;
     nb += p.n_nonfinite;
   }
-  mcb_trial_stats st;
   st.n_samples = n + nb;
   st.n_nonfinite = nb;
   st.nonfinite_warning = double(nb) > MCB_NONFINITE_WARN_FRACTION * double(n + nb) ? 1u : 0u;
@@ -134,7 +225,7 @@ static const Table& table() {
 
 static const Entry* entry(int family, int dim, int variant) {
   if (family < 0 || family > 3 || dim < 1 || dim > int(MCB_MAX_DIM) || variant < 0 ||
-      variant > 15)
+      variant > 31)
     return nullptr;
   const Entry* e = &table().e[family][dim][variant];
   return e->direct ? e : nullptr;

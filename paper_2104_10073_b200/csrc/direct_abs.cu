@@ -10,6 +10,8 @@ static void put_abs(Table& t) {
   t.put<F, D, 0>();
   t.put<F, D, kUnitDomain>();
   t.put<F, D, kSafe>();
+  t.put_run<F, D, 0>();
+  t.put_run<F, D, kSafe>();
 }
 
 void register_abs(Table& t) {

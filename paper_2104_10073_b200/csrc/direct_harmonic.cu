@@ -17,6 +17,11 @@ static void put_harmonic(Table& t) {
   t.put<F, D, kNoShift | kUnitCoef>();
   t.put<F, D, kNoShift | kUnitCoef | kUnitDomain>();
   t.put<F, D, kSafe>();
+  t.put_run<F, D, 0>();
+  t.put_run<F, D, kUnitCoef>();
+  t.put_run<F, D, kNoShift>();
+  t.put_run<F, D, kNoShift | kUnitCoef>();
+  t.put_run<F, D, kSafe>();
 }
 
 void register_harmonic(Table& t) {

@@ -13,6 +13,9 @@ static void put_vec(Table& t) {
   t.put<F, D, kNoShift>();
   t.put<F, D, kNoShift | kUnitDomain>();
   t.put<F, D, kSafe>();
+  t.put_run<F, D, 0>();
+  t.put_run<F, D, kNoShift>();
+  t.put_run<F, D, kSafe>();
 }
 
 void register_harmonic_vec(Table& t) {

@@ -51,19 +51,28 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
   constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
   constexpr bool SAFE = (V & kSafe) != 0;
   constexpr bool NOSHIFT = (V & kNoShift) != 0;
+  constexpr bool STRAT = (V & kStrat) != 0;
   constexpr bool HARM = FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC;
   constexpr bool TABLE = HARM && !SAFE;
 
   const uint64_t tile = tile0 + blockIdx.x;
   const uint32_t fi = __ldg(tile_fn + tile);
-  const FnDesc f = fns[fi];  // uniform; ptxas keeps only the fields this variant reads
+  FnDesc f = fns[fi];  // uniform; ptxas keeps only the fields this variant reads
 
   const uint32_t rem = uint32_t(tile - f.tile_base);
   const uint32_t trial = rem / f.n_chunks;
-  const uint32_t chunk = rem - trial * f.n_chunks;
-  const uint32_t count =
-      (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
-                                : MCB_CHUNK_SIZE;
+  const uint32_t chunk = rem - trial * f.n_chunks;  // STRAT: cell * cpc + chunk in cell
+  uint32_t count;
+  if (STRAT) {
+    // stratified_mc cell `cell`: direct_mc over grid_cell(domain, k, cell) with
+    // spc samples and chunk keys cell * cpc + c (ref src/batch.cpp:255-275)
+    const uint32_t cell = chunk / f.cpc, cc = chunk - cell * f.cpc;
+    count = (cc + 1 == f.cpc) ? f.spc - cc * MCB_CHUNK_SIZE : MCB_CHUNK_SIZE;
+    dev::grid_cell<D>(f, f.strat_k, cell, SAFE ? 1.0 : dev::kTwoM64);
+  } else {
+    count = (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
+                                      : MCB_CHUNK_SIZE;
+  }
   const uint32_t pairs = (count + 1) >> 1;
   const PhiloxPrefix P =
       dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
@@ -71,6 +80,20 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
   if (TABLE) {
     build_trig_table<UNIT_COEF>(ab, f.a, f.b);
     __syncthreads();
+  }
+  // STRAT: per-tile shift = f(first sample of the tile); tiles merge by
+  // Chan's formula in k_combine, so cells (often near-constant) keep an
+  // exactly zero variance when f is constant on them.
+  if (STRAT && !NOSHIFT) {
+    __shared__ double s_shift;
+    if (threadIdx.x == 0) {
+      double st0, st1;
+      dev::gen_pair<FAM, D, false, SAFE>(f, P, 0ull, st0, st1);
+      const double f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, st0);
+      s_shift = finite64(f0) ? f0 : 0.0;
+    }
+    __syncthreads();
+    f.shift = s_shift;
   }
 
   double s1 = 0.0, s2 = 0.0;
@@ -139,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
     TilePartial p;
     p.s1 = t1;
     p.s2 = t2;
+    p.shift = NOSHIFT ? 0.0 : f.shift;
     p.n_nonfinite = SAFE ? tb : 0u;
     p.n_finite = count - p.n_nonfinite;
     part[tile] = p;
@@ -181,11 +205,17 @@ struct Entry {
 };
 
 struct Table {
-  Entry e[4][MCB_MAX_DIM + 1][16];
+  Entry e[4][MCB_MAX_DIM + 1][32];
   template <int FAM, int D, int V>
   void put() {
     e[FAM][D][V].direct = k_direct<FAM, D, V>;
     e[FAM][D][V].eval = k_debug_eval<FAM, D, V>;
+  }
+  // stratified variants: the fused kernel only (cell values are tested
+  // through the direct variants on the cell rectangle)
+  template <int FAM, int D, int V>
+  void put_run() {
+    e[FAM][D][V | kStrat].direct = k_direct<FAM, D, V | kStrat>;
   }
 };
 

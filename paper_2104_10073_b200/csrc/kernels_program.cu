@@ -157,20 +157,38 @@ __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
                                                const uint32_t* __restrict__ code,
                                                const double* __restrict__ consts, uint32_t slots) {
   constexpr bool UNIT_DOM = (V & kUnitDomain) != 0;
+  constexpr bool STRAT = (V & kStrat) != 0;
   const uint64_t tile = tile0 + blockIdx.x;
   const uint32_t fi = __ldg(tile_fn + tile);
-  const FnDesc f = fns[fi];
+  FnDesc f = fns[fi];
   const uint32_t rem = uint32_t(tile - f.tile_base);
   const uint32_t trial = rem / f.n_chunks;
-  const uint32_t chunk = rem - trial * f.n_chunks;
-  const uint32_t count =
-      (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
-                                : MCB_CHUNK_SIZE;
+  const uint32_t chunk = rem - trial * f.n_chunks;  // STRAT: cell * cpc + chunk in cell
+  uint32_t count;
+  if (STRAT) {  // see k_direct: cells of stratified_mc (ref src/batch.cpp:255-275)
+    const uint32_t cell = chunk / f.cpc, cc = chunk - cell * f.cpc;
+    count = (cc + 1 == f.cpc) ? f.spc - cc * MCB_CHUNK_SIZE : MCB_CHUNK_SIZE;
+    dev::grid_cell<D>(f, f.strat_k, cell, 1.0);
+  } else {
+    count = (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
+                                      : MCB_CHUNK_SIZE;
+  }
   const uint32_t pairs = (count + 1) >> 1;
   const PhiloxPrefix P =
       dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
   __shared__ double params[prog::kMaxParams];
   const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  if (STRAT) {  // per-tile shift = f(first sample of the tile)
+    __shared__ double s_shift;
+    if (threadIdx.x == 0) {
+      gen_points<D, false>(f, P, 0, m.X);
+      interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+      const double f0 = m.S[0];
+      s_shift = finite64(f0) ? f0 : 0.0;
+    }
+    __syncthreads();
+    f.shift = s_shift;
+  }
 
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
@@ -214,6 +232,7 @@ __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
     TilePartial p;
     p.s1 = t1;
     p.s2 = t2;
+    p.shift = f.shift;
     p.n_nonfinite = tb;
     p.n_finite = count - tb;
     part[tile] = p;
@@ -255,11 +274,12 @@ struct ProgEntry {
 };
 
 struct ProgTable {
-  ProgEntry e[MCB_MAX_DIM + 1][2];
+  ProgEntry e[MCB_MAX_DIM + 1][3];  // general domain, unit domain, stratified
   template <int D>
   void put() {
     e[D][0] = {k_program<D, kSafe>, k_program_eval<D, kSafe>};
     e[D][1] = {k_program<D, kSafe | kUnitDomain>, k_program_eval<D, kSafe | kUnitDomain>};
+    e[D][2] = {k_program<D, kSafe | kStrat>, k_program_eval<D, kSafe>};
   }
   ProgTable() {
     put<1>();
@@ -290,7 +310,7 @@ static cudaError_t ensure_smem_optin() {
   if (done.count(dev)) return cudaSuccess;
   const ProgTable& t = prog_table();
   for (int d = 1; d <= int(MCB_MAX_DIM); ++d)
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < 3; ++v) {
       const int smem = int(program_smem_bytes(prog::kMaxDepth, d));
       if ((e = cudaFuncSetAttribute(t.e[d][v].run, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem)) != cudaSuccess)
@@ -305,7 +325,7 @@ static cudaError_t ensure_smem_optin() {
 
 static const ProgEntry* prog_entry(int dim, int variant) {
   if (dim < 1 || dim > int(MCB_MAX_DIM)) return nullptr;
-  return &prog_table().e[dim][(variant & kUnitDomain) ? 1 : 0];
+  return &prog_table().e[dim][(variant & kStrat) ? 2 : (variant & kUnitDomain) ? 1 : 0];
 }
 
 cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const uint32_t* tile_fn,

@@ -31,8 +31,10 @@ enum Variant : int {
   kSafe = 4,        // plain parameters, libdevice sincos, non-finite samples
                     // counted and skipped (used when the host cannot prove
                     // the FAST preconditions, see capi.cpp prepare())
-  kNoShift = 8      // harmonic FAST: accumulate f itself (the host proved the
+  kNoShift = 8,     // harmonic FAST: accumulate f itself (the host proved the
                     // integrand far from constant, so no cancellation)
+  kStrat = 16       // STRATIFIED method: tiles are (trial, cell, chunk), the
+                    // cell rectangle is derived on the device (grid_cell)
 };
 
 // One kernel launch = one (family, dim, variant) group of integrands whose

@@ -111,7 +111,7 @@ std::vector<double> sample_uniform(const HyperRect& rect, const StreamKey& key, 
 
 // ---- integrand specs --------------------------------------------------------
 
-const char* method_name(Method) { return "direct"; }
+const char* method_name(Method m) { return m == Method::Stratified ? "stratified" : "direct"; }
 
 CompiledSource compile_program(const std::string& source, std::size_t dim,
                                const std::map<std::string, double>& params) {
@@ -160,7 +160,25 @@ mcb_integrand to_descriptor(const IntegrandSpec& s, std::uint32_t integrand_inde
     d.low[j] = s.domain.low[j];
     d.high[j] = s.domain.high[j];
   }
+  if (s.method == Method::Stratified) {
+    const RefineConfig rc = s.method_config.value_or(RefineConfig{});
+    d.method = MCB_METHOD_STRATIFIED;
+    d.cells_per_dim = rc.init_cells_per_dim;
+    d.cell_cap = rc.cell_cap;
+  }
   return d;
+}
+
+StratifiedPlan stratified_plan(const IntegrandSpec& spec) {
+  IntegrandSpec s = spec;
+  s.method = Method::Stratified;
+  mcb_integrand d = to_descriptor(s, 0);
+  StratifiedPlan p;
+  uint64_t n = 0;
+  if (mcb_stratified_plan(&d, &p.cells_per_dim, &n, &p.samples_per_cell) != MCB_OK)
+    throw std::invalid_argument(mcb_last_error());  // reference: CellBudgetExceeded
+  p.n_cells = n;
+  return p;
 }
 
 std::string IntegrandSpec::source() const {
@@ -293,6 +311,8 @@ McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const S
                       &st));
   if (st.status == MCB_TRIAL_ALL_NONFINITE)
     throw AllSamplesNonFinite("every sample evaluated to NaN or infinity");
+  if (st.status == MCB_TRIAL_DEAD_CELL)
+    throw AllSamplesNonFinite("cell " + std::to_string(st.detail) + " produced no finite sample");
   return to_estimate(st);
 }
 
@@ -355,7 +375,7 @@ BatchResult run_batch(const JobSpec& job) {
   double total_cost = 0.0;
   std::vector<double> cost(n);
   for (std::size_t i = 0; i < n; ++i) {
-    cost[i] = double(descs[i].n_samples) * double(descs[i].dim);
+    cost[i] = double(out[i * trials].n_samples) * double(descs[i].dim);
     total_cost += cost[i];
   }
   for (std::size_t i = 0; i < n; ++i) {
@@ -371,7 +391,10 @@ BatchResult run_batch(const JobSpec& job) {
         r.nonfinite_warning |= e.nonfinite_warning;
         ok.push_back(e);
       } else if (first_error.empty()) {
-        first_error = "trial " + std::to_string(t) + ": every sample evaluated to NaN or infinity";
+        first_error = "trial " + std::to_string(t) + ": " +
+                      (st.status == MCB_TRIAL_DEAD_CELL
+                           ? "cell " + std::to_string(st.detail) + " produced no finite sample"
+                           : std::string("every sample evaluated to NaN or infinity"));
       }
     }
     const std::size_t need = trials >= 2 ? 2 : 1;  // src/batch.cpp:320

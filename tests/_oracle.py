@@ -55,6 +55,9 @@ def load():
         "orc_summarize_trials": (i32, [P(TrialStats), u32, P(dbl), P(dbl), P(u32)]),
         "orc_run_direct": (i32, [P(Integrand), sz, u64, u32, i32, vp]),
         "orc_harmonic_k": (dbl, [u32]),
+        "orc_stratified_mc": (i32, [P(Integrand), u64, u32, u64, P(TrialStats)]),
+        "orc_stratified_plan": (i32, [P(Integrand), P(u32), P(u64), P(u32)]),
+        "orc_grid_cell": (None, [P(Integrand), u32, u64, P(dbl), P(dbl)]),
         "orc_harmonic_closed_form": (dbl, [dbl, u32]),
     }
     for name, (res, args) in sig.items():

@@ -146,7 +146,25 @@ def main():
     g["harmonic_job"] = {"k": [H(k) for k in ks], "seed": seed.value, "trials": trials.value,
                          "analytic": [H(ref.ref_analytic_harmonic(n)) for n in range(1, 101)]}
 
-    # 6. arbitrary DSL programs (the GPU interpreter's parity anchors)
+    # 6. stratified method: run_batch Stratified branch (src/batch.cpp:255-275)
+    strat = []
+    sfns = [mcb.stratify(mcb.harmonic(workloads.harmonic_k(3), 4, unit_coeffs=True, n_samples=100_000, index=0)),
+            mcb.stratify(mcb.make_integrand(mcb.FAMILY_ABS2, 2, a=1.3, low=[-0.4, 0.0], high=[1.0, 1.4],
+                                            n_samples=50_000, index=1), cells_per_dim=3),
+            mcb.stratify(mcb.make_integrand(mcb.FAMILY_ABS3, 3, n_samples=30_000, index=2), cells_per_dim=1),
+            mcb.stratify(mcb.make_integrand(mcb.FAMILY_HARMONIC_VEC, 3, k=[2.0, -1.0, 0.5], a=1.5, b=0.5,
+                                            low=[-1, 0, 0.5], high=[1, 2, 1.5], n_samples=200_003, index=3)),
+            mcb.stratify(mcb.harmonic(0.0, 2, a=3.0, b=1.0, low=[0, 0], high=[1, 2], n_samples=5_000, index=4),
+                         cells_per_dim=5),
+            mcb.stratify(mcb.harmonic(1.7, 2, a=1.0, b=-2.0, n_samples=300_000, index=5), cells_per_dim=2)]
+    out, mean, sd, ok, _ = _oracle.ref_run_batch(sfns, 31, 3, workers=0)
+    for i, f in enumerate(sfns):
+        strat.append({"desc": desc_json(f), "method": int(f.method), "cells_per_dim": int(f.cells_per_dim),
+                      "per_trial": [stats_json(_as_stats(out[i, t])) for t in range(3)],
+                      "mean": H(float(mean[i])), "trial_stddev": H(float(sd[i])), "ok": int(ok[i])})
+    g["stratified"] = {"seed": 31, "trials": 3, "cases": strat}
+
+    # 7. arbitrary DSL programs (the GPU interpreter's parity anchors)
     g["programs"] = make_program_goldens(ref)
 
     with open(os.path.join(HERE, "golden.json"), "w") as fh:

@@ -29,10 +29,11 @@ def fx(h):
     return float.fromhex(h)
 
 
-def desc_from(d):
+def desc_from(d, method=0, cells_per_dim=0):
     import paper_2104_10073_b200 as mcb
     f = mcb.Integrand()
     f.family, f.dim, f.integrand_index, f.flags = d["family"], d["dim"], d["integrand_index"], d["flags"]
+    f.method, f.cells_per_dim = method, cells_per_dim
     f.n_samples = d["n_samples"]
     f.a, f.b = fx(d["a"]), fx(d["b"])
     for j in range(8):
@@ -120,6 +121,19 @@ def test_run_batch_matches_reference_golden(golden, oracle):
             oracle.orc_summarize_trials(per.ctypes.data_as(ctypes.POINTER(TrialStats)), rb["trials"],
                                         ctypes.byref(mean), ctypes.byref(sd), ctypes.byref(nok))
             assert mean.value == fx(rb["mean"][i]) and sd.value == fx(rb["trial_stddev"][i])
+
+
+def test_stratified_matches_reference_golden(golden, oracle):
+    """stratified_mc / combine_cells (ref src/estimator.cpp:94-182) bit-exact."""
+    sg = golden["stratified"]
+    fns = [desc_from(c["desc"], c["method"], c["cells_per_dim"]) for c in sg["cases"]]
+    out = _oracle.run_direct(fns, sg["seed"], sg["trials"], n_threads=4)
+    for i, c in enumerate(sg["cases"]):
+        for t in range(sg["trials"]):
+            e = c["per_trial"][t]
+            assert out[i, t]["value"] == fx(e["value"]), (i, t)
+            assert out[i, t]["std_error"] == fx(e["std_error"]), (i, t)
+            assert int(out[i, t]["n_samples"]) == e["n_samples"]
 
 
 def test_worker_count_invariance(oracle):

@@ -34,7 +34,16 @@ def main():
         out.append(prog)  # keep alive
         return out, seed, trials
 
+    def stratified(fns_seed_trials):
+        fns, seed, trials = fns_seed_trials
+        for f in fns:
+            mcb.stratify(f)
+        return fns, seed, trials
+
     builders = {
+        "c1_strat": lambda: stratified(w.c1()),
+        "c2_strat": lambda: stratified(w.c2()),
+        "c3_strat": lambda: stratified(w.c3()),
         "c1_program": lambda: as_program(w.c1()),
         "c2_program": lambda: as_program(w.c2()),
         "c1": lambda: w.c1(),
