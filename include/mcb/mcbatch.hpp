@@ -75,7 +75,7 @@ enum class Family {
   Program = MCB_FAMILY_PROGRAM            // any DSL source (`program_source`)
 };
 
-enum class Method { Direct, Stratified };
+enum class Method { Direct, Stratified, Tree };  // Tree: parsed, rejected by validate
 const char* method_name(Method m);
 
 // include/mcbatch/estimator.hpp:39-46 (stratified uses init_cells_per_dim
@@ -100,7 +100,7 @@ struct IntegrandSpec {
   std::uint64_t n_samples = 10000;
   Method method = Method::Direct;
   std::optional<RefineConfig> method_config;
-  std::string program_source;  // Family::Program: the DSL source
+  std::string program_source;  // the DSL source (Family::Program; kept verbatim by from_source)
 
   // Exact reference DSL source of this descriptor.
   std::string source() const;
@@ -114,9 +114,13 @@ struct IntegrandSpec {
 struct JobSpec {
   std::uint64_t seed = 0;
   std::uint32_t trials = 1;
-  std::vector<int> devices;  // empty = {0}
+  std::uint32_t workers = 0;  // GPUs to use when `devices` is empty (0 = all visible)
+  std::vector<int> devices;   // explicit CUDA ordinals
   std::vector<IntegrandSpec> integrands;
 };
+
+// Devices for a worker count: 0..workers-1, or every visible GPU for 0.
+std::vector<int> devices_for_workers(std::uint32_t workers);
 
 struct Violation {
   std::string integrand;  // empty for job-level problems

@@ -255,6 +255,30 @@ int ref_direct_mc_source(const char* source, std::uint32_t dim, const char* cons
   }
 }
 
+// read_job + write_job (src/job_io.cpp:114-142): re-serialise a job file.
+int ref_job_roundtrip(const char* in_path, const char* out_path) {
+  try {
+    JobSpec job = read_job(in_path);
+    write_job(job, out_path);
+    return int(job.integrands.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// read_results + write_results (src/job_io.cpp:207-284): re-serialise a CSV.
+int ref_results_roundtrip(const char* in_path, const char* out_path) {
+  try {
+    auto rows = read_results(in_path);
+    write_results(rows, out_path);
+    return int(rows.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 double ref_harmonic_closed_form(double k) { return harmonic_closed_form(k); }
 double ref_analytic_harmonic(std::uint32_t n) { return analytic_harmonic(n); }
 

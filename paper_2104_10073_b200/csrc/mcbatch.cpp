@@ -111,7 +111,17 @@ std::vector<double> sample_uniform(const HyperRect& rect, const StreamKey& key, 
 
 // ---- integrand specs --------------------------------------------------------
 
-const char* method_name(Method m) { return m == Method::Stratified ? "stratified" : "direct"; }
+const char* method_name(Method m) {
+  return m == Method::Stratified ? "stratified" : (m == Method::Tree ? "tree" : "direct");
+}
+
+std::vector<int> devices_for_workers(std::uint32_t workers) {
+  int n = mcb_device_count();
+  if (workers > 0 && int(workers) < n) n = int(workers);
+  std::vector<int> d;
+  for (int i = 0; i < std::max(n, 1); ++i) d.push_back(i);
+  return d;
+}
 
 CompiledSource compile_program(const std::string& source, std::size_t dim,
                                const std::map<std::string, double>& params) {
@@ -182,7 +192,7 @@ StratifiedPlan stratified_plan(const IntegrandSpec& spec) {
 }
 
 std::string IntegrandSpec::source() const {
-  if (family == Family::Program) return program_source;
+  if (family == Family::Program || !program_source.empty()) return program_source;
   mcb_integrand d = to_descriptor(*this, 0);
   std::string s(mcb_to_dsl(&d, nullptr, 0), '\0');
   mcb_to_dsl(&d, s.data(), s.size());
@@ -217,10 +227,11 @@ IntegrandSpec IntegrandSpec::from_source(std::string name, const std::string& so
     t.params["a"] = c.a1 ? 1.0 : 2.0;  // only selects the printed form
     if (c.f == Family::Abs2 && dim < 2) continue;
     if (c.f == Family::Abs3 && dim < 3) continue;
+    t.program_source.clear();
     if (strip(t.source()) == want) {
       s.family = c.f;
       s.unit_coeffs = c.unit;
-      if (c.a1) s.params["a"] = 1.0;
+      s.program_source = source;  // keep the caller's text (job-file round trips)
       return s;
     }
   }
@@ -251,6 +262,8 @@ std::vector<Violation> validate(const JobSpec& job) {
   ProgramCache programs;
   for (std::size_t i = 0; i < job.integrands.size(); ++i) {
     const IntegrandSpec& s = job.integrands[i];
+    if (s.method == Method::Tree)
+      out.push_back({s.name, "method 'tree' is not supported by the GPU backend (direct, stratified)"});
     const mcb_program* prog = nullptr;
     if (s.family == Family::Program) {
       try {
@@ -366,8 +379,8 @@ BatchResult run_batch(const JobSpec& job) {
   }
   std::vector<mcb_trial_stats> out(n * trials);
   double seconds = 0.0;
-  const int* devs = job.devices.empty() ? nullptr : job.devices.data();
-  check(mcb_run_direct(descs.data(), n, job.seed, trials, devs, int(job.devices.size()), out.data(),
+  const std::vector<int> devices = job.devices.empty() ? devices_for_workers(job.workers) : job.devices;
+  check(mcb_run_direct(descs.data(), n, job.seed, trials, devices.data(), int(devices.size()), out.data(),
                        &seconds));
 
   BatchResult result;

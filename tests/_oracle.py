@@ -155,6 +155,8 @@ def load_ref():
         "ref_direct_mc_source": (i32, [ctypes.c_char_p, u32, P(ctypes.c_char_p), P(dbl), sz, P(dbl), P(dbl),
                                        u64, u64, u32, u32, u64, P(TrialStats)]),
         "ref_analytic_harmonic": (dbl, [u32]),
+        "ref_job_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
+        "ref_results_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
