@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define MCB_ABI_VERSION 1u
+#define MCB_ABI_VERSION 2u
 
 #if defined(__GNUC__)
 #define MCB_API __attribute__((visibility("default")))
@@ -75,6 +75,10 @@ typedef enum mcb_family {
 typedef struct mcb_program mcb_program;
 
 #define MCB_FLAG_UNIT_COEFFS 0x1u
+/* TREE: samples_per_cell, max_depth and sigma_multiplier are taken as given;
+ * without the flag they are the RefineConfig defaults 2048, 6, 1.0
+ * (include/mcbatch/estimator.hpp:40-47), so a zeroed descriptor is valid. */
+#define MCB_FLAG_REFINE_CONFIG 0x2u
 
 /* One integrand = one reference IntegrandSpec (include/mcbatch/batch.hpp:22-31)
  * restricted to Method::Direct and a family descriptor.  `integrand_index` is
@@ -94,21 +98,36 @@ typedef struct mcb_integrand {
   double high[MCB_MAX_DIM]; /* HyperRect high */
   const mcb_program* program; /* PROGRAM family only (not owned) */
   uint32_t method;          /* mcb_method (reference Method, include/mcbatch/batch.hpp:18) */
-  uint32_t cells_per_dim;   /* STRATIFIED: k (0 = auto, ref src/batch.cpp:41-54) */
-  uint64_t cell_cap;        /* STRATIFIED: max k^d cells (0 = 1e6, RefineConfig::cell_cap) */
+  uint32_t cells_per_dim;   /* STRATIFIED: k (0 = auto, ref src/batch.cpp:41-54);
+                               TREE: RefineConfig::init_cells_per_dim (0 = auto) */
+  uint64_t cell_cap;        /* STRATIFIED/TREE: max k^d cells (0 = 1e6, RefineConfig::cell_cap) */
+  /* TREE only (RefineConfig, include/mcbatch/estimator.hpp:40-47; the
+   * refinement budget total_budget is n_samples, as run_batch sets it,
+   * src/batch.cpp:278-279).  Read only with MCB_FLAG_REFINE_CONFIG. */
+  uint32_t samples_per_cell;
+  uint32_t max_depth;
+  double sigma_multiplier;
 } mcb_integrand;
 
 typedef enum mcb_method {
   MCB_METHOD_DIRECT = 0,     /* direct_mc, ref src/estimator.cpp:75-92 */
-  MCB_METHOD_STRATIFIED = 1  /* k^d grid cells, direct_mc per cell, combine_cells
+  MCB_METHOD_STRATIFIED = 1, /* k^d grid cells, direct_mc per cell, combine_cells
                                 (ref src/estimator.cpp:94-182, src/batch.cpp:255-275) */
+  MCB_METHOD_TREE = 2        /* adaptive longest-edge refinement, tree_refine
+                                (ref src/estimator.cpp:184-318, src/batch.cpp:276-289):
+                                host-driven rounds, each round's cells batched
+                                across every tree (integrand, trial) onto the GPU */
 } mcb_method;
 
 enum {
   MCB_TRIAL_OK = 0,
   MCB_TRIAL_ALL_NONFINITE = 1, /* every sample non-finite (AllSamplesNonFinite) */
-  MCB_TRIAL_DEAD_CELL = 2      /* stratified: cell `detail` had no finite sample
+  MCB_TRIAL_DEAD_CELL = 2,     /* stratified: cell `detail` had no finite sample
                                   (ref src/batch.cpp:176-180) */
+  MCB_TRIAL_CELL_BUDGET = 3,   /* tree: auto initial grid exceeds cell_cap
+                                  (CellBudgetExceeded, src/estimator.cpp:94-105) */
+  MCB_TRIAL_CHUNK_RANGE = 4    /* tree: a cell's chunk index passed 2^32-1
+                                  (std::out_of_range, src/sampling.cpp:80-81) */
 };
 
 /* Per-(integrand, trial) result = reference McEstimate
@@ -122,8 +141,20 @@ typedef struct mcb_trial_stats {
   uint32_t status;    /* MCB_TRIAL_* */
   uint32_t nonfinite_warning;
   uint32_t detail;    /* MCB_TRIAL_DEAD_CELL: index of the first dead cell */
-  uint32_t n_cells;   /* stratified: cells combined (1 for direct) */
+  uint32_t n_cells;   /* stratified: cells combined; tree: leaves (1 for direct) */
+  uint32_t budget_exhausted; /* tree: McEstimate::budget_exhausted */
+  uint32_t max_depth;        /* tree: deepest leaf (0 otherwise) */
 } mcb_trial_stats;
+
+/* One leaf of a refined tree (reference StratumNode,
+ * include/mcbatch/estimator.hpp:33-38). */
+typedef struct mcb_leaf {
+  double low[MCB_MAX_DIM];
+  double high[MCB_MAX_DIM];
+  mcb_trial_stats estimate; /* status ALL_NONFINITE for a dead leaf */
+  uint32_t depth;
+  uint32_t reserved;
+} mcb_leaf;
 
 /* One validation problem (reference Violation, include/mcbatch/batch.hpp:40-44).
  * integrand = -1 for job-level problems. */
@@ -185,8 +216,9 @@ MCB_API size_t mcb_program_param_name(const mcb_program* program, uint32_t i, ch
                                       size_t cap);
 
 /* ---- the hot path -------------------------------------------------------- */
-/* run_batch Direct branch (src/batch.cpp:195-333): every integrand, every
- * trial t in [0, trials), StreamKey {seed, integrand_index, t, chunk}.
+/* run_batch (src/batch.cpp:195-333): every integrand, every trial t in
+ * [0, trials), StreamKey {seed, integrand_index, t, chunk}, by each
+ * integrand's method (DIRECT, STRATIFIED, TREE).
  * `out` is n_fns*trials, row-major by integrand.  Devices: `devices` lists
  * CUDA ordinals (NULL/0 = device 0); one host thread per entry, integrands
  * sharded by mcb_partition; results are byte-identical for any device list.
@@ -200,6 +232,15 @@ MCB_API mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64
  * {seed, fn->integrand_index, trial, chunk_base}, on `device`. */
 MCB_API mcb_status mcb_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
                          uint64_t chunk_base, int device, mcb_trial_stats* out);
+
+/* tree_refine (src/estimator.cpp:212-318) for one integrand (method TREE,
+ * n_samples = total_budget) and key base {seed, fn->integrand_index, trial,
+ * chunk_base}.  Cells are estimated on `device`.  `leaves` (may be NULL)
+ * receives up to `leaf_cap` leaves in the reference's leaf order; *n_leaves
+ * (may be NULL) the total.  A dead trial is reported through out->status. */
+MCB_API mcb_status mcb_tree_refine(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
+                                   uint64_t chunk_base, int device, mcb_trial_stats* out,
+                                   mcb_leaf* leaves, size_t leaf_cap, size_t* n_leaves);
 
 /* ---- device-resident plans (descriptors stay in HBM; async on a stream) -- */
 typedef struct mcb_plan mcb_plan;

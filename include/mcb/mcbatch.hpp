@@ -12,8 +12,9 @@
 //  * JobSpec::workers (CPU threads) becomes JobSpec::devices (CUDA ordinals).
 //    Results are byte-identical for any device list, the analogue of the
 //    reference's worker invariance (tests/test_batch.cpp:91-121).
-//  * Method::Direct and Method::Stratified run on the GPU; Method::Tree
-//    (sequential adaptive refinement) is not implemented.
+//  * Every method runs on the GPU: Direct and Stratified as fused launches,
+//    Tree as host-driven refinement rounds whose cells (of every tree in the
+//    batch) are estimated by the same fused kernels (csrc/tree.cpp).
 #pragma once
 
 #include <cstdint>
@@ -75,11 +76,11 @@ enum class Family {
   Program = MCB_FAMILY_PROGRAM            // any DSL source (`program_source`)
 };
 
-enum class Method { Direct, Stratified, Tree };  // Tree: parsed, rejected by validate
+enum class Method { Direct, Stratified, Tree };
 const char* method_name(Method m);
 
-// include/mcbatch/estimator.hpp:39-46 (stratified uses init_cells_per_dim
-// and cell_cap; the tree fields are carried for source compatibility)
+// include/mcbatch/estimator.hpp:40-47 (stratified uses init_cells_per_dim
+// and cell_cap; run_batch sets a tree's total_budget to n_samples)
 struct RefineConfig {
   std::uint32_t init_cells_per_dim = 0;  // 0 = auto (k^d <= min(4096, n/2))
   std::uint32_t samples_per_cell = 2048;
@@ -196,6 +197,21 @@ std::vector<TrialSummary> parameter_scan(const IntegrandSpec& tmpl, const std::s
 // src/estimator.cpp:75-92; throws AllSamplesNonFinite like the reference.
 McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const StreamKey& key_base,
                      int device = 0);
+
+// include/mcbatch/estimator.hpp:33-38
+struct StratumNode {
+  HyperRect cell;
+  McEstimate estimate;
+  std::uint32_t depth = 0;
+};
+struct CellBudgetExceeded : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// src/estimator.cpp:212-318 with the config's total_budget; cells estimated on
+// `device`.  Throws AllSamplesNonFinite / CellBudgetExceeded like the reference.
+McEstimate tree_refine(const IntegrandSpec& spec, const RefineConfig& config, const StreamKey& key_base,
+                       std::vector<StratumNode>* leaves_out = nullptr, int device = 0);
 
 // src/estimator.cpp:320-337
 TrialSummary summarize_trials(std::vector<McEstimate> per_trial);

@@ -367,6 +367,172 @@ ORC_EXPORT int orc_stratified_mc(const mcb_integrand* fn, uint64_t seed, uint32_
   return 0;
 }
 
+/* ---- tree: src/estimator.cpp:184-318, src/batch.cpp:276-289 ------------- */
+
+typedef struct {
+  double low[MCB_MAX_DIM], high[MCB_MAX_DIM];
+  mcb_trial_stats est;
+  uint32_t depth;
+} orc_leaf;
+
+/* estimate_cell lambda, src/estimator.cpp:238-253: direct_mc of the cell with
+ * key chunk next_chunk; AllSamplesNonFinite becomes a dead leaf.  Returns -1
+ * when the chunk index leaves 32 bits (UniformStream throws). */
+static int orc_estimate_cell(const mcb_integrand* fn, orc_leaf* l, uint32_t spc, uint64_t cpc,
+                             uint64_t seed, uint32_t trial, uint64_t* next_chunk, uint64_t* used) {
+  if (*next_chunk + cpc - 1 > 0xFFFFFFFFull) return -1;
+  mcb_integrand cell = *fn;
+  cell.method = MCB_METHOD_DIRECT;
+  cell.n_samples = spc;
+  memcpy(cell.low, l->low, sizeof cell.low);
+  memcpy(cell.high, l->high, sizeof cell.high);
+  uint64_t key_chunk = *next_chunk;
+  *next_chunk += cpc;
+  *used += spc;
+  if (orc_direct_mc(&cell, seed, trial, key_chunk, &l->est) != 0) return -1;
+  if (l->est.status != MCB_TRIAL_OK) {
+    memset(&l->est, 0, sizeof l->est);
+    l->est.status = MCB_TRIAL_ALL_NONFINITE;
+    l->est.n_samples = spc;
+    l->est.n_nonfinite = spc;
+    l->est.nonfinite_warning = 1;
+  }
+  return 0;
+}
+
+/* tree_refine, src/estimator.cpp:212-318, with RefineConfig from the
+ * descriptor (MCB_FLAG_REFINE_CONFIG; total_budget = n_samples as run_batch
+ * sets it, src/batch.cpp:278).  Leaves (may be NULL) in the reference's order. */
+ORC_EXPORT int orc_tree_refine(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
+                               uint64_t chunk_base, mcb_trial_stats* out, mcb_leaf* leaves_out,
+                               size_t cap, size_t* n_leaves) {
+  const uint32_t d = fn->dim;
+  uint32_t spc_cfg = 2048, max_depth = 6;
+  double sigma = 1.0;
+  if (fn->flags & MCB_FLAG_REFINE_CONFIG) {
+    spc_cfg = fn->samples_per_cell;
+    max_depth = fn->max_depth;
+    sigma = fn->sigma_multiplier;
+  }
+  const uint64_t budget = fn->n_samples;
+  const uint64_t cell_cap = fn->cell_cap ? fn->cell_cap : 1000000ull;
+  const uint32_t spc = spc_cfg > 2 ? spc_cfg : 2;
+  memset(out, 0, sizeof *out);
+  uint32_t k = fn->cells_per_dim;
+  if (k == 0) {
+    k = auto_cells_per_dim(d, 4096);
+    while (k > 1) {
+      uint64_t cells = cell_grid_size(k, d, cell_cap);
+      if (cells == 0) { out->status = MCB_TRIAL_CELL_BUDGET; return 0; }
+      if (cells * spc <= budget / 2) break;
+      --k;
+    }
+  }
+  const uint64_t n_cells = cell_grid_size(k, d, cell_cap);
+  if (n_cells == 0) { out->status = MCB_TRIAL_CELL_BUDGET; return 0; }
+  const uint64_t cpc = orc_chunk_count(spc);
+  uint64_t next_chunk = chunk_base, used = 0;
+  int exhausted = 0;
+  size_t n = 0, capl = (size_t)n_cells + 16;
+  orc_leaf* lv = (orc_leaf*)malloc(sizeof(orc_leaf) * capl);
+  size_t* sel = NULL;
+  if (!lv) return -1;
+  mcb_integrand rect = *fn;
+  for (uint64_t c = 0; c < n_cells; ++c, ++n) {
+    memset(&lv[n], 0, sizeof lv[n]);
+    orc_grid_cell(&rect, k, c, lv[n].low, lv[n].high);
+    if (orc_estimate_cell(fn, &lv[n], spc, cpc, seed, trial, &next_chunk, &used) != 0) {
+      free(lv);
+      out->status = MCB_TRIAL_CHUNK_RANGE;
+      return 0;
+    }
+  }
+  while (!exhausted) {
+    double mean_err = 0.0;
+    for (size_t i = 0; i < n; ++i) mean_err += lv[i].est.std_error;
+    mean_err /= (double)n;
+    double ss = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      double dlt = lv[i].est.std_error - mean_err;
+      ss += dlt * dlt;
+    }
+    double sd = n > 1 ? sqrt(ss / (double)(n - 1)) : 0.0;
+    double threshold = mean_err + sigma * sd;
+    size_t n_sel = 0;
+    free(sel);
+    sel = (size_t*)malloc(sizeof(size_t) * n);
+    for (size_t i = 0; i < n; ++i)
+      if (lv[i].depth < max_depth && lv[i].est.std_error > 0 && lv[i].est.std_error > threshold)
+        sel[n_sel++] = i;
+    if (n_sel == 0) break;
+    for (size_t s = 0; s < n_sel; ++s) {
+      size_t idx = sel[s];
+      if (used + 2ull * spc > budget) { exhausted = 1; break; }
+      if (n + 1 > capl) {
+        capl *= 2;
+        lv = (orc_leaf*)realloc(lv, sizeof(orc_leaf) * capl);
+      }
+      /* split_longest_edge, src/estimator.cpp:192-210 */
+      orc_leaf lo = lv[idx], hi = lv[idx];
+      uint32_t axis = 0;
+      double best = -1.0;
+      for (uint32_t j = 0; j < d; ++j) {
+        double w = lv[idx].high[j] - lv[idx].low[j];
+        if (w > best) { best = w; axis = j; }
+      }
+      double mid = lv[idx].low[axis] + 0.5 * (lv[idx].high[axis] - lv[idx].low[axis]);
+      lo.high[axis] = mid;
+      hi.low[axis] = mid;
+      lo.depth = hi.depth = lv[idx].depth + 1;
+      if (orc_estimate_cell(fn, &lo, spc, cpc, seed, trial, &next_chunk, &used) != 0 ||
+          orc_estimate_cell(fn, &hi, spc, cpc, seed, trial, &next_chunk, &used) != 0) {
+        free(lv); free(sel);
+        out->status = MCB_TRIAL_CHUNK_RANGE;
+        return 0;
+      }
+      lv[idx] = lo;
+      lv[n++] = hi;
+    }
+  }
+  free(sel);
+  /* combine_cells over the leaves, src/estimator.cpp:145-159 and :299-306 */
+  double value = 0.0, var = 0.0;
+  uint64_t ns = 0, nn = 0, finite = 0;
+  uint32_t depth = 0;
+  for (size_t i = 0; i < n; ++i) {
+    value += lv[i].est.value;
+    var += lv[i].est.std_error * lv[i].est.std_error;
+    ns += lv[i].est.n_samples;
+    nn += lv[i].est.n_nonfinite;
+    finite += lv[i].est.n_samples - lv[i].est.n_nonfinite;
+    if (lv[i].depth > depth) depth = lv[i].depth;
+  }
+  out->n_samples = ns;
+  out->n_nonfinite = nn;
+  out->n_cells = (uint32_t)n;
+  out->max_depth = depth;
+  out->budget_exhausted = (uint32_t)exhausted;
+  if (finite == 0) {
+    out->status = MCB_TRIAL_ALL_NONFINITE;
+  } else {
+    out->status = MCB_TRIAL_OK;
+    out->value = value;
+    out->std_error = sqrt(var);
+    out->nonfinite_warning = (double)nn > MCB_NONFINITE_WARN_FRACTION * (double)ns;
+  }
+  if (out->status != MCB_TRIAL_OK) n = 0; /* leaves_out is written only on return */
+  if (n_leaves) *n_leaves = n;
+  for (size_t i = 0; leaves_out && i < n && i < cap; ++i) {
+    memset(&leaves_out[i], 0, sizeof leaves_out[i]);
+    memcpy(leaves_out[i].low, lv[i].low, sizeof lv[i].low);
+    memcpy(leaves_out[i].high, lv[i].high, sizeof lv[i].high);
+    leaves_out[i].estimate = lv[i].est;
+    leaves_out[i].depth = lv[i].depth;
+  }
+  free(lv);
+  return 0;
+}
+
 /* summarize_trials, src/estimator.cpp:320-337, over the OK trials only
  * (run_batch collects the successful ones, src/batch.cpp:309-318). */
 ORC_EXPORT int orc_summarize_trials(const mcb_trial_stats* per_trial, uint32_t n,
@@ -391,7 +557,7 @@ ORC_EXPORT int orc_summarize_trials(const mcb_trial_stats* per_trial, uint32_t n
   return 0;
 }
 
-/* run_batch Direct branch, src/batch.cpp:195-333: (integrand, trial) units
+/* run_batch, src/batch.cpp:195-333, every method: (integrand, trial) units
  * with StreamKey {seed, integrand_index, trial, 0} drained by a thread pool
  * (src/batch.cpp:150-168).  Results do not depend on n_threads. */
 typedef struct {
@@ -416,7 +582,9 @@ static void* orc_worker(void* arg) {
     uint32_t t = (uint32_t)(u % p->trials);
     int rc = p->fns[i].method == MCB_METHOD_STRATIFIED
                  ? orc_stratified_mc(&p->fns[i], p->seed, t, 0, &p->out[u])
-                 : orc_direct_mc(&p->fns[i], p->seed, t, 0, &p->out[u]);
+                 : p->fns[i].method == MCB_METHOD_TREE
+                       ? orc_tree_refine(&p->fns[i], p->seed, t, 0, &p->out[u], NULL, 0, NULL)
+                       : orc_direct_mc(&p->fns[i], p->seed, t, 0, &p->out[u]);
     if (rc != 0) p->failed = 1;
   }
   return NULL;

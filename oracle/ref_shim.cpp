@@ -12,6 +12,7 @@
 // No reference source is copied here: this file only includes the public
 // headers (include/mcbatch/*.hpp) and calls the public API.
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -70,6 +71,21 @@ void fill(const McEstimate& e, mcb_trial_stats* st) {
   st->n_nonfinite = e.n_nonfinite;
   st->status = MCB_TRIAL_OK;
   st->nonfinite_warning = e.nonfinite_warning ? 1u : 0u;
+  st->budget_exhausted = e.budget_exhausted ? 1u : 0u;
+}
+
+// RefineConfig of a STRATIFIED / TREE descriptor (mcb.h field meanings).
+RefineConfig refine_config_of(const mcb_integrand& f) {
+  RefineConfig rc;
+  rc.init_cells_per_dim = f.cells_per_dim;
+  if (f.cell_cap) rc.cell_cap = f.cell_cap;
+  if (f.flags & MCB_FLAG_REFINE_CONFIG) {
+    rc.samples_per_cell = f.samples_per_cell;
+    rc.max_depth = f.max_depth;
+    rc.sigma_multiplier = f.sigma_multiplier;
+  }
+  rc.total_budget = f.n_samples;
+  return rc;
 }
 
 }  // namespace
@@ -160,13 +176,10 @@ int ref_run_batch(const char* const* sources, const mcb_integrand* fns, std::siz
       s.domain = rect_of(fns[i].dim, fns[i].low, fns[i].high);
       s.params = params_of(fns[i]);
       s.n_samples = fns[i].n_samples;
-      s.method = fns[i].method == MCB_METHOD_STRATIFIED ? Method::Stratified : Method::Direct;
-      if (s.method == Method::Stratified) {
-        RefineConfig rc;
-        rc.init_cells_per_dim = fns[i].cells_per_dim;
-        if (fns[i].cell_cap) rc.cell_cap = fns[i].cell_cap;
-        s.method_config = rc;
-      }
+      s.method = fns[i].method == MCB_METHOD_STRATIFIED
+                     ? Method::Stratified
+                     : (fns[i].method == MCB_METHOD_TREE ? Method::Tree : Method::Direct);
+      if (s.method != Method::Direct) s.method_config = refine_config_of(fns[i]);
       job.integrands.push_back(std::move(s));
     }
     BatchResult br = run_batch(job);
@@ -247,6 +260,49 @@ int ref_direct_mc_source(const char* source, std::uint32_t dim, const char* cons
       out->status = MCB_TRIAL_ALL_NONFINITE;
       out->n_samples = n_samples;
       out->n_nonfinite = n_samples;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// tree_refine (src/estimator.cpp:212-318) of an arbitrary source, config from
+// the descriptor; leaves (cap entries) in the reference's order.
+int ref_tree_refine_source(const char* source, const mcb_integrand* f, const char* const* names,
+                           const double* values, std::size_t n_params, std::uint64_t seed,
+                           std::uint32_t trial, std::uint64_t chunk_base, mcb_trial_stats* out,
+                           mcb_leaf* leaves, std::size_t cap, std::size_t* n_leaves) {
+  try {
+    std::map<std::string, double> pm;
+    for (std::size_t i = 0; i < n_params; ++i) pm[names[i]] = values[i];
+    std::vector<std::string> nm;
+    std::vector<double> vals;
+    for (auto& [k, v] : pm) { nm.push_back(k); vals.push_back(v); }
+    CompiledProgram prog = compile(parse(source), f->dim, nm);
+    std::memset(out, 0, sizeof *out);
+    std::vector<StratumNode> lv;
+    try {
+      fill(tree_refine(prog, vals, rect_of(f->dim, f->low, f->high), refine_config_of(*f),
+                       StreamKey{seed, f->integrand_index, trial, chunk_base}, &lv),
+           out);
+    } catch (const AllSamplesNonFinite&) {
+      out->status = MCB_TRIAL_ALL_NONFINITE;
+    } catch (const CellBudgetExceeded&) {
+      out->status = MCB_TRIAL_CELL_BUDGET;
+    }
+    out->n_cells = std::uint32_t(lv.size());
+    if (n_leaves) *n_leaves = lv.size();
+    for (std::size_t i = 0; i < lv.size() && i < cap; ++i) {
+      std::memset(&leaves[i], 0, sizeof leaves[i]);
+      for (std::uint32_t j = 0; j < f->dim; ++j) {
+        leaves[i].low[j] = lv[i].cell.low[j];
+        leaves[i].high[j] = lv[i].cell.high[j];
+      }
+      fill(lv[i].estimate, &leaves[i].estimate);
+      leaves[i].depth = lv[i].depth;
+      out->max_depth = std::max(out->max_depth, lv[i].depth);
     }
     return 0;
   } catch (const std::exception& e) {

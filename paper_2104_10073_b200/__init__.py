@@ -7,7 +7,8 @@ raises, and compute calls without a B200 return ``MCB_ERR_NO_DEVICE``.
 
 Reference correspondence (``/root/reference/proj``):
 ``run_direct`` ~ ``run_batch`` Direct branch (src/batch.cpp:195-333),
-``direct_mc`` ~ src/estimator.cpp:75-92, ``debug_points`` ~ ``sample_uniform``
+``direct_mc`` ~ src/estimator.cpp:75-92, ``tree_refine`` ~ src/estimator.cpp:212-318,
+``debug_points`` ~ ``sample_uniform``
 (src/sampling.cpp:102-112), ``make_harmonic_job`` ~ src/job_io.cpp:355-376.
 """
 from __future__ import annotations
@@ -32,14 +33,18 @@ FAMILY_ABS2 = 2
 FAMILY_ABS3 = 3
 FAMILY_PROGRAM = 4
 FLAG_UNIT_COEFFS = 1
+FLAG_REFINE_CONFIG = 2
 MAX_PARAMS = 8
 
 TRIAL_OK = 0
 TRIAL_ALL_NONFINITE = 1
 TRIAL_DEAD_CELL = 2
+TRIAL_CELL_BUDGET = 3
+TRIAL_CHUNK_RANGE = 4
 
 METHOD_DIRECT = 0
 METHOD_STRATIFIED = 1
+METHOD_TREE = 2
 
 STATUS = {0: "MCB_OK", 1: "MCB_ERR_INVALID_ARGUMENT", 2: "MCB_ERR_VALIDATION", 3: "MCB_ERR_CUDA",
           4: "MCB_ERR_NO_DEVICE", 5: "MCB_ERR_OUT_OF_RANGE", 6: "MCB_ERR_BUFFER_TOO_SMALL"}
@@ -59,7 +64,8 @@ class Integrand(ctypes.Structure):
                 ("k", ctypes.c_double * MAX_DIM), ("low", ctypes.c_double * MAX_DIM),
                 ("high", ctypes.c_double * MAX_DIM), ("program", ctypes.c_void_p),
                 ("method", ctypes.c_uint32), ("cells_per_dim", ctypes.c_uint32),
-                ("cell_cap", ctypes.c_uint64)]
+                ("cell_cap", ctypes.c_uint64), ("samples_per_cell", ctypes.c_uint32),
+                ("max_depth", ctypes.c_uint32), ("sigma_multiplier", ctypes.c_double)]
 
 
 class TrialStats(ctypes.Structure):
@@ -67,7 +73,14 @@ class TrialStats(ctypes.Structure):
     _fields_ = [("value", ctypes.c_double), ("std_error", ctypes.c_double),
                 ("n_samples", ctypes.c_uint64), ("n_nonfinite", ctypes.c_uint64),
                 ("status", ctypes.c_uint32), ("nonfinite_warning", ctypes.c_uint32),
-                ("detail", ctypes.c_uint32), ("n_cells", ctypes.c_uint32)]
+                ("detail", ctypes.c_uint32), ("n_cells", ctypes.c_uint32),
+                ("budget_exhausted", ctypes.c_uint32), ("max_depth", ctypes.c_uint32)]
+
+
+class Leaf(ctypes.Structure):
+    """``mcb_leaf`` = reference StratumNode (include/mcbatch/estimator.hpp:33-38)."""
+    _fields_ = [("low", ctypes.c_double * MAX_DIM), ("high", ctypes.c_double * MAX_DIM),
+                ("estimate", TrialStats), ("depth", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class Violation(ctypes.Structure):
@@ -83,7 +96,8 @@ class PlanInfo(ctypes.Structure):
 
 TRIAL_DTYPE = np.dtype([("value", "<f8"), ("std_error", "<f8"), ("n_samples", "<u8"),
                         ("n_nonfinite", "<u8"), ("status", "<u4"), ("nonfinite_warning", "<u4"),
-                        ("detail", "<u4"), ("n_cells", "<u4")])
+                        ("detail", "<u4"), ("n_cells", "<u4"), ("budget_exhausted", "<u4"),
+                        ("max_depth", "<u4")])
 assert TRIAL_DTYPE.itemsize == ctypes.sizeof(TrialStats)
 
 # Every symbol include/mcb/mcb.h declares (checked by tests/test_abi.py).
@@ -93,7 +107,7 @@ ABI_SYMBOLS = [
     "mcb_direct_mc", "mcb_plan_create", "mcb_plan_launch", "mcb_plan_download",
     "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
     "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
-    "mcb_program_param_name", "mcb_stratified_plan",
+    "mcb_program_param_name", "mcb_stratified_plan", "mcb_tree_refine",
 ]
 
 
@@ -131,6 +145,7 @@ def _load() -> ctypes.CDLL:
         "mcb_program_info": (i32, [vp, P(u32), P(u32), P(u32)]),
         "mcb_program_param_name": (sz, [vp, u32, ctypes.c_char_p, sz]),
         "mcb_stratified_plan": (i32, [P(Integrand), P(u32), P(u64), P(u32)]),
+        "mcb_tree_refine": (i32, [P(Integrand), u64, u32, u64, i32, P(TrialStats), P(Leaf), sz, P(sz)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -273,6 +288,20 @@ def stratify(f: Integrand, cells_per_dim: int = 0, cell_cap: int = 0) -> Integra
     return f
 
 
+def tree(f: Integrand, *, init_cells_per_dim: int = 0, samples_per_cell: int = 2048,
+         max_depth: int = 6, sigma_multiplier: float = 1.0, cell_cap: int = 0) -> Integrand:
+    """Switch an integrand to the adaptive tree method (ref src/estimator.cpp:212-318);
+    its n_samples is the refinement budget.  Defaults = RefineConfig's."""
+    f.method = METHOD_TREE
+    f.cells_per_dim = init_cells_per_dim
+    f.cell_cap = cell_cap
+    f.flags |= FLAG_REFINE_CONFIG
+    f.samples_per_cell = samples_per_cell
+    f.max_depth = max_depth
+    f.sigma_multiplier = sigma_multiplier
+    return f
+
+
 def stratified_plan(f: Integrand):
     """(cells_per_dim, n_cells, samples_per_cell) — ref src/batch.cpp:41-54."""
     k, n, spc = ctypes.c_uint32(), ctypes.c_uint64(), ctypes.c_uint32()
@@ -317,6 +346,22 @@ def direct_mc(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, devi
     st = TrialStats()
     _check(lib.mcb_direct_mc(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st)))
     return st
+
+
+def tree_refine(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, device: int = 0,
+                leaves: bool = False):
+    """tree_refine (ref src/estimator.cpp:212-318) of one integrand on the GPU.
+    Returns the TrialStats, or (TrialStats, [Leaf]) with ``leaves=True``."""
+    st = TrialStats()
+    n = ctypes.c_size_t()
+    _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), None, 0,
+                               ctypes.byref(n)))
+    if not leaves:
+        return st
+    buf = (Leaf * max(1, n.value))()
+    _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), buf,
+                               n.value, ctypes.byref(n)))
+    return st, list(buf[:n.value])
 
 
 class Plan:

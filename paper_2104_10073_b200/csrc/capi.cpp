@@ -5,6 +5,7 @@
 //   mcb_validate        validate                 src/batch.cpp:62-120
 //   mcb_run_direct      run_batch (Direct)       src/batch.cpp:195-333
 //   mcb_direct_mc       direct_mc                src/estimator.cpp:75-92
+//   mcb_tree_refine     tree_refine              src/estimator.cpp:212-318 (tree.cpp)
 //   mcb_summarize_trials summarize_trials        src/estimator.cpp:320-337
 //   mcb_stream_key      UniformStream key        src/sampling.cpp:84-87
 //   mcb_volume          HyperRect::volume        src/sampling.cpp:16-20
@@ -29,6 +30,7 @@
 #include "mcb/mcb.h"
 #include "mcb_internal.hpp"
 #include "program.hpp"
+#include "tree.hpp"
 
 // Opaque compiled program of the C-ABI.
 struct mcb_program {
@@ -260,10 +262,19 @@ void violations_of(const mcb_integrand& f, uint32_t trials,
   if ((f.flags & MCB_FLAG_UNIT_COEFFS) &&
       !(f.family == MCB_FAMILY_HARMONIC && f.a == 1.0 && f.b == 1.0))
     out.push_back("unit-coefficient flag needs the harmonic family with a = b = 1");
-  if (f.flags & ~MCB_FLAG_UNIT_COEFFS) out.push_back("unknown flag bits");
-  if (f.method > MCB_METHOD_STRATIFIED) {
+  if (f.flags & ~(MCB_FLAG_UNIT_COEFFS | MCB_FLAG_REFINE_CONFIG)) out.push_back("unknown flag bits");
+  if (f.method > MCB_METHOD_TREE) {
     out.push_back("unknown method " + std::to_string(f.method));
     return;
+  }
+  if (f.method == MCB_METHOD_TREE) {  // src/batch.cpp:94-106
+    const mcb::tree::Config rc = mcb::tree::config_of(f);
+    uint64_t cells;
+    if (rc.init_cells_per_dim > 0 && f.dim >= 1 && f.dim <= MCB_MAX_DIM &&
+        !cell_grid_size(rc.init_cells_per_dim, f.dim, rc.cell_cap, cells))
+      out.push_back("cell grid exceeds configured cap");
+    if (!(rc.sigma_multiplier == rc.sigma_multiplier)) out.push_back("sigma_multiplier is NaN");
+    return;  // chunk indices are checked per cell at run time (MCB_TRIAL_CHUNK_RANGE)
   }
   uint64_t nc = chunk_count(f.n_samples);
   if (stratified(f) && f.dim >= 1 && f.dim <= MCB_MAX_DIM) {
@@ -495,10 +506,15 @@ struct HostPlan {
   uint64_t n_tiles = 0, total_samples = 0, philox_blocks = 0;
 };
 
+// chunk_bases / trial_bases (may be NULL): per-integrand key bases overriding
+// chunk_base / trial_base (the tree driver's cell batches).
 mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
-                           uint32_t chunk_base, uint32_t trial_base, HostPlan& hp) {
+                           uint32_t chunk_base, uint32_t trial_base, HostPlan& hp,
+                           const uint32_t* chunk_bases = nullptr, const uint32_t* trial_bases = nullptr) {
   std::vector<Prepared> prep(n_fns);
-  for (size_t i = 0; i < n_fns; ++i) prep[i] = prepare(fns[i], seed, chunk_base, trial_base);
+  for (size_t i = 0; i < n_fns; ++i)
+    prep[i] = prepare(fns[i], seed, chunk_bases ? chunk_bases[i] : chunk_base,
+                      trial_bases ? trial_bases[i] : trial_base);
   std::vector<size_t> order(n_fns);
   std::iota(order.begin(), order.end(), size_t(0));
   std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
@@ -665,9 +681,10 @@ cudaError_t grow_pinned(T*& p, size_t& cap, size_t need) {
 
 // One shard of mcb_run_direct on one device (synchronous).
 mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
-                     int device, mcb_trial_stats* out) {
+                     int device, mcb_trial_stats* out, const uint32_t* chunk_bases = nullptr,
+                     const uint32_t* trial_bases = nullptr) {
   HostPlan hp;
-  mcb_status st = build_host_plan(fns, n_fns, seed, trials, 0, 0, hp);
+  mcb_status st = build_host_plan(fns, n_fns, seed, trials, 0, 0, hp, chunk_bases, trial_bases);
   if (st != MCB_OK) return st;
   DeviceCtx& c = device_ctx(device);
   std::lock_guard<std::mutex> lock(c.mu);
@@ -710,6 +727,10 @@ mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t see
                             uint32_t trial_base, mcb_plan** out) {
   mcb_status st = validate_for_run(fns, n_fns, trials);
   if (st != MCB_OK) return st;
+  for (size_t i = 0; i < n_fns; ++i)
+    if (fns[i].method == MCB_METHOD_TREE)
+      return fail(MCB_ERR_INVALID_ARGUMENT,
+                  "method tree has no static plan (use mcb_run_direct or mcb_tree_refine)");
   if (chunk_base) {
     for (size_t i = 0; i < n_fns; ++i)
       if (uint64_t(chunk_base) + chunk_count(fns[i].n_samples) - 1 > 0xFFFFFFFFull)
@@ -775,6 +796,63 @@ void lpt(const mcb_integrand* fns, size_t n, uint32_t trials, int shards, uint32
     shard_of[i] = uint32_t(best);
     load[best] += cost[i];
   }
+}
+
+// Shards integrands over `devs` by LPT, one host thread per device; results
+// land in `out` (n_fns * trials) by integrand.  Byte-identical for any list.
+mcb_status run_sharded(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
+                       const std::vector<int>& devs, mcb_trial_stats* out, const uint32_t* chunk_bases,
+                       const uint32_t* trial_bases) {
+  std::vector<uint32_t> shard(n_fns, 0);
+  lpt(fns, n_fns, trials, int(devs.size()), shard.data());
+  std::vector<mcb_status> status(devs.size(), MCB_OK);
+  std::vector<std::string> errors(devs.size());
+  auto work = [&](size_t w) {
+    std::vector<size_t> mine;
+    for (size_t i = 0; i < n_fns; ++i)
+      if (shard[i] == w) mine.push_back(i);
+    if (mine.empty()) return;
+    std::vector<mcb_integrand> sub(mine.size());
+    std::vector<uint32_t> cb, tb;
+    for (size_t r = 0; r < mine.size(); ++r) sub[r] = fns[mine[r]];
+    if (chunk_bases)
+      for (size_t i : mine) cb.push_back(chunk_bases[i]);
+    if (trial_bases)
+      for (size_t i : mine) tb.push_back(trial_bases[i]);
+    std::vector<mcb_trial_stats> res(sub.size() * trials);
+    const mcb_status s = run_shard(sub.data(), sub.size(), seed, trials, devs[w], res.data(),
+                                   chunk_bases ? cb.data() : nullptr, trial_bases ? tb.data() : nullptr);
+    status[w] = s;
+    if (s != MCB_OK) {
+      errors[w] = g_last_error;
+      return;
+    }
+    for (size_t r = 0; r < mine.size(); ++r)
+      std::memcpy(out + mine[r] * trials, res.data() + r * trials, sizeof(mcb_trial_stats) * trials);
+  };
+  if (devs.size() == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (size_t w = 0; w < devs.size(); ++w) pool.emplace_back(work, w);
+    for (auto& th : pool) th.join();
+  }
+  for (size_t w = 0; w < devs.size(); ++w)
+    if (status[w] != MCB_OK) return fail(status[w], "device " + std::to_string(devs[w]) + ": " + errors[w]);
+  return MCB_OK;
+}
+
+// One round of tree cells: 1-trial direct units with per-cell key bases.
+mcb_status run_cells(const std::vector<mcb::tree::CellJob>& jobs, uint64_t seed, const std::vector<int>& devs,
+                     mcb_trial_stats* out) {
+  std::vector<mcb_integrand> fns(jobs.size());
+  std::vector<uint32_t> cb(jobs.size()), tb(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    fns[i] = jobs[i].fn;
+    cb[i] = uint32_t(jobs[i].chunk_base);  // < 2^32: checked by the driver
+    tb[i] = jobs[i].trial;
+  }
+  return run_sharded(fns.data(), fns.size(), seed, 1, devs, out, cb.data(), tb.data());
 }
 
 }  // namespace
@@ -945,38 +1023,55 @@ mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
     if ((st = check_device(d)) != MCB_OK) return st;
 
   const auto t0 = std::chrono::steady_clock::now();
-  std::vector<uint32_t> shard(n_fns, 0);
-  lpt(fns, n_fns, trials, int(devs.size()), shard.data());
-  std::vector<mcb_status> status(devs.size(), MCB_OK);
-  std::vector<std::string> errors(devs.size());
-  auto work = [&](size_t w) {
-    std::vector<size_t> mine;
-    for (size_t i = 0; i < n_fns; ++i)
-      if (shard[i] == w) mine.push_back(i);
-    if (mine.empty()) return;
-    std::vector<mcb_integrand> sub(mine.size());
-    for (size_t r = 0; r < mine.size(); ++r) sub[r] = fns[mine[r]];
+  std::vector<size_t> plain, trees;
+  for (size_t i = 0; i < n_fns; ++i) (fns[i].method == MCB_METHOD_TREE ? trees : plain).push_back(i);
+  if (!plain.empty()) {  // direct + stratified: one sharded launch set
+    std::vector<mcb_integrand> sub(plain.size());
+    for (size_t r = 0; r < plain.size(); ++r) sub[r] = fns[plain[r]];
     std::vector<mcb_trial_stats> res(sub.size() * trials);
-    const mcb_status s = run_shard(sub.data(), sub.size(), seed, trials, devs[w], res.data());
-    status[w] = s;
-    if (s != MCB_OK) {
-      errors[w] = g_last_error;
-      return;
-    }
-    for (size_t r = 0; r < mine.size(); ++r)
-      std::memcpy(out + mine[r] * trials, res.data() + r * trials, sizeof(mcb_trial_stats) * trials);
-  };
-  if (devs.size() == 1) {
-    work(0);
-  } else {
-    std::vector<std::thread> pool;
-    for (size_t w = 0; w < devs.size(); ++w) pool.emplace_back(work, w);
-    for (auto& th : pool) th.join();
+    if ((st = run_sharded(sub.data(), sub.size(), seed, trials, devs, res.data(), nullptr, nullptr)) != MCB_OK)
+      return st;
+    for (size_t r = 0; r < plain.size(); ++r)
+      std::memcpy(out + plain[r] * trials, res.data() + r * trials, sizeof(mcb_trial_stats) * trials);
+  }
+  if (!trees.empty()) {  // tree: lock-step rounds over every (integrand, trial) tree
+    std::vector<mcb::tree::TreeTask> tasks;
+    tasks.reserve(trees.size() * trials);
+    for (size_t i : trees)
+      for (uint32_t t = 0; t < trials; ++t)
+        tasks.push_back(mcb::tree::TreeTask{&fns[i], t, 0, out + i * trials + t, nullptr});
+    if ((st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellJob>& jobs,
+                                              mcb_trial_stats* o) { return run_cells(jobs, seed, devs, o); })) !=
+        MCB_OK)
+      return st;
   }
   const auto t1 = std::chrono::steady_clock::now();
   if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
-  for (size_t w = 0; w < devs.size(); ++w)
-    if (status[w] != MCB_OK) return fail(status[w], "device " + std::to_string(devs[w]) + ": " + errors[w]);
+  return MCB_OK;
+}
+
+mcb_status mcb_tree_refine(const mcb_integrand* fn, uint64_t seed, uint32_t trial, uint64_t chunk_base,
+                           int device, mcb_trial_stats* out, mcb_leaf* leaves, size_t leaf_cap,
+                           size_t* n_leaves) {
+  if (!fn || !out) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  // tree_refine itself has no validation step: a grid past the cap is a
+  // CellBudgetExceeded result (MCB_TRIAL_CELL_BUDGET), not a job error.
+  mcb_integrand f = *fn;
+  f.method = MCB_METHOD_DIRECT;
+  mcb_status st = validate_for_run(&f, 1, 1);
+  if (st != MCB_OK) return st;
+  f.method = MCB_METHOD_TREE;
+  if ((st = check_device(device)) != MCB_OK) return st;
+  std::vector<mcb_leaf> lv;
+  std::vector<mcb::tree::TreeTask> tasks{mcb::tree::TreeTask{&f, trial, chunk_base, out, &lv}};
+  const std::vector<int> devs{device};
+  st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellJob>& jobs, mcb_trial_stats* o) {
+    return run_cells(jobs, seed, devs, o);
+  });
+  if (st != MCB_OK) return st;
+  if (n_leaves) *n_leaves = lv.size();
+  if (leaves)
+    std::memcpy(leaves, lv.data(), sizeof(mcb_leaf) * std::min(leaf_cap, lv.size()));
   return MCB_OK;
 }
 
@@ -988,8 +1083,10 @@ mcb_status mcb_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
     return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
   // One (integrand, trial) unit: a 1-trial plan whose key base is
   // {seed, integrand_index, trial, chunk_base}.
+  mcb_integrand f = *fn;  // direct_mc ignores the spec's method
+  f.method = MCB_METHOD_DIRECT;
   mcb_plan* plan = nullptr;
-  mcb_status st = plan_create_impl(fn, 1, seed, 1, device, uint32_t(chunk_base), trial, &plan);
+  mcb_status st = plan_create_impl(&f, 1, seed, 1, device, uint32_t(chunk_base), trial, &plan);
   if (st != MCB_OK) return st;
   st = plan_launch_impl(plan, nullptr);
   if (st == MCB_OK) st = plan_download_impl(plan, out, nullptr);

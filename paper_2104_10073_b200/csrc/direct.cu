@@ -95,6 +95,8 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
   mcb_trial_stats st;
   st.detail = 0;
   st.n_cells = 1;
+  st.budget_exhausted = 0;
+  st.max_depth = 0;
   if (F.strat_k > 0) {
     double value = 0.0, var = 0.0;
     uint64_t n_all = 0, nn_all = 0;

@@ -170,11 +170,17 @@ mcb_integrand to_descriptor(const IntegrandSpec& s, std::uint32_t integrand_inde
     d.low[j] = s.domain.low[j];
     d.high[j] = s.domain.high[j];
   }
-  if (s.method == Method::Stratified) {
+  if (s.method == Method::Stratified || s.method == Method::Tree) {
     const RefineConfig rc = s.method_config.value_or(RefineConfig{});
-    d.method = MCB_METHOD_STRATIFIED;
+    d.method = s.method == Method::Tree ? MCB_METHOD_TREE : MCB_METHOD_STRATIFIED;
     d.cells_per_dim = rc.init_cells_per_dim;
     d.cell_cap = rc.cell_cap;
+    if (s.method == Method::Tree) {  // total_budget = n_samples (src/batch.cpp:278)
+      d.flags |= MCB_FLAG_REFINE_CONFIG;
+      d.samples_per_cell = rc.samples_per_cell;
+      d.max_depth = rc.max_depth;
+      d.sigma_multiplier = rc.sigma_multiplier;
+    }
   }
   return d;
 }
@@ -262,8 +268,6 @@ std::vector<Violation> validate(const JobSpec& job) {
   ProgramCache programs;
   for (std::size_t i = 0; i < job.integrands.size(); ++i) {
     const IntegrandSpec& s = job.integrands[i];
-    if (s.method == Method::Tree)
-      out.push_back({s.name, "method 'tree' is not supported by the GPU backend (direct, stratified)"});
     const mcb_program* prog = nullptr;
     if (s.family == Family::Program) {
       try {
@@ -307,7 +311,18 @@ static McEstimate to_estimate(const mcb_trial_stats& t) {
   e.n_samples = t.n_samples;
   e.n_nonfinite = t.n_nonfinite;
   e.nonfinite_warning = t.nonfinite_warning != 0;
+  e.budget_exhausted = t.budget_exhausted != 0;
   return e;
+}
+
+// The reference's exception text of a failed trial (src/batch.cpp:172-190).
+static std::string trial_error(const mcb_trial_stats& st) {
+  switch (st.status) {
+    case MCB_TRIAL_DEAD_CELL: return "cell " + std::to_string(st.detail) + " produced no finite sample";
+    case MCB_TRIAL_CELL_BUDGET: return "cell grid exceeds configured cap";
+    case MCB_TRIAL_CHUNK_RANGE: return "chunk_index exceeds 32 bits";
+    default: return "every sample evaluated to NaN or infinity";
+  }
 }
 
 McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const StreamKey& key_base,
@@ -326,6 +341,42 @@ McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const S
     throw AllSamplesNonFinite("every sample evaluated to NaN or infinity");
   if (st.status == MCB_TRIAL_DEAD_CELL)
     throw AllSamplesNonFinite("cell " + std::to_string(st.detail) + " produced no finite sample");
+  return to_estimate(st);
+}
+
+McEstimate tree_refine(const IntegrandSpec& spec, const RefineConfig& config, const StreamKey& key_base,
+                       std::vector<StratumNode>* leaves_out, int device) {  // :212-318
+  if (spec.domain.dim() != spec.dim) throw std::invalid_argument("program/domain dimension mismatch");
+  IntegrandSpec s = spec;
+  s.method = Method::Tree;
+  s.method_config = config;
+  ProgramCache programs;
+  const mcb_program* prog = s.family == Family::Program ? programs.get(s) : nullptr;
+  mcb_integrand d = to_descriptor(s, key_base.integrand_index, prog);
+  d.n_samples = config.total_budget;
+  mcb_trial_stats st{};
+  size_t n = 0;
+  check(mcb_tree_refine(&d, key_base.global_seed, key_base.trial_index, key_base.chunk_index, device, &st,
+                        nullptr, 0, &n));
+  std::vector<mcb_leaf> lv(n);
+  if (leaves_out)
+    check(mcb_tree_refine(&d, key_base.global_seed, key_base.trial_index, key_base.chunk_index, device, &st,
+                          lv.data(), lv.size(), &n));
+  if (st.status == MCB_TRIAL_CELL_BUDGET) throw CellBudgetExceeded("cell grid exceeds configured cap");
+  if (st.status == MCB_TRIAL_CHUNK_RANGE) throw std::out_of_range("chunk_index exceeds 32 bits");
+  if (st.status == MCB_TRIAL_ALL_NONFINITE)
+    throw AllSamplesNonFinite("every sample evaluated to NaN or infinity");
+  if (leaves_out) {
+    leaves_out->clear();
+    for (const mcb_leaf& l : lv) {
+      StratumNode node;
+      node.cell.low.assign(l.low, l.low + s.dim);
+      node.cell.high.assign(l.high, l.high + s.dim);
+      node.estimate = to_estimate(l.estimate);
+      node.depth = l.depth;
+      leaves_out->push_back(std::move(node));
+    }
+  }
   return to_estimate(st);
 }
 
@@ -402,12 +453,10 @@ BatchResult run_batch(const JobSpec& job) {
       if (st.status == MCB_TRIAL_OK) {
         McEstimate e = to_estimate(st);
         r.nonfinite_warning |= e.nonfinite_warning;
+        r.budget_exhausted |= e.budget_exhausted;
         ok.push_back(e);
       } else if (first_error.empty()) {
-        first_error = "trial " + std::to_string(t) + ": " +
-                      (st.status == MCB_TRIAL_DEAD_CELL
-                           ? "cell " + std::to_string(st.detail) + " produced no finite sample"
-                           : std::string("every sample evaluated to NaN or infinity"));
+        first_error = "trial " + std::to_string(t) + ": " + trial_error(st);
       }
     }
     const std::size_t need = trials >= 2 ? 2 : 1;  // src/batch.cpp:320

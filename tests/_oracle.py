@@ -34,7 +34,7 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    from paper_2104_10073_b200 import Integrand, TrialStats  # struct layouts only
+    from paper_2104_10073_b200 import Integrand, Leaf, TrialStats  # struct layouts only
     build()
     lib = ctypes.CDLL(ORACLE_SO)
     P = ctypes.POINTER
@@ -59,6 +59,7 @@ def load():
         "orc_stratified_plan": (i32, [P(Integrand), P(u32), P(u64), P(u32)]),
         "orc_grid_cell": (None, [P(Integrand), u32, u64, P(dbl), P(dbl)]),
         "orc_harmonic_closed_form": (dbl, [dbl, u32]),
+        "orc_tree_refine": (i32, [P(Integrand), u64, u32, u64, P(TrialStats), P(Leaf), sz, P(sz)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -105,6 +106,40 @@ def eval_points(f, pts):
     return out
 
 
+def tree_refine(f, seed, trial=0, chunk_base=0):
+    """orc_tree_refine: (TrialStats, [Leaf]) — ref src/estimator.cpp:212-318."""
+    from paper_2104_10073_b200 import Leaf, TrialStats
+    lib = load()
+    st = TrialStats()
+    n = ctypes.c_size_t()
+    if lib.orc_tree_refine(ctypes.byref(f), seed, trial, chunk_base, ctypes.byref(st), None, 0,
+                           ctypes.byref(n)) != 0:
+        raise ValueError("oracle tree_refine failed")
+    buf = (Leaf * max(1, n.value))()
+    lib.orc_tree_refine(ctypes.byref(f), seed, trial, chunk_base, ctypes.byref(st), buf, n.value,
+                        ctypes.byref(n))
+    return st, list(buf[:n.value])
+
+
+def ref_tree_refine(source, f, params, seed, trial=0, chunk_base=0):
+    """The reference's own tree_refine of `source` (params: name -> value)."""
+    from paper_2104_10073_b200 import Leaf, TrialStats
+    lib = load_ref()
+    if lib is None:
+        raise FileNotFoundError(REF_SO)
+    names = list(params)
+    cn = (ctypes.c_char_p * max(1, len(names)))(*[n.encode() for n in names])
+    cv = (ctypes.c_double * max(1, len(names)))(*[params[n] for n in names])
+    st = TrialStats()
+    n = ctypes.c_size_t()
+    cap = 1 << 16
+    buf = (Leaf * cap)()
+    if lib.ref_tree_refine_source(source.encode(), ctypes.byref(f), cn, cv, len(names), seed, trial,
+                                  chunk_base, ctypes.byref(st), buf, cap, ctypes.byref(n)) != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return st, list(buf[:min(n.value, cap)])
+
+
 def direct_mc(f, seed, trial=0, chunk_base=0):
     from paper_2104_10073_b200 import TrialStats
     lib = load()
@@ -137,7 +172,7 @@ def load_ref():
         return _ref
     if not os.path.exists(REF_SO):
         return None
-    from paper_2104_10073_b200 import Integrand, TrialStats
+    from paper_2104_10073_b200 import Integrand, Leaf, TrialStats
     lib = ctypes.CDLL(REF_SO)
     P = ctypes.POINTER
     u32, u64, dbl, i32, sz = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_int, ctypes.c_size_t
@@ -157,6 +192,8 @@ def load_ref():
         "ref_analytic_harmonic": (dbl, [u32]),
         "ref_job_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
         "ref_results_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
+        "ref_tree_refine_source": (i32, [ctypes.c_char_p, P(Integrand), P(ctypes.c_char_p), P(dbl), sz, u64,
+                                         u32, u64, P(TrialStats), P(Leaf), sz, P(sz)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

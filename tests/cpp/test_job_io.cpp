@@ -209,6 +209,15 @@ static void run_command_exit_codes() {
   std::ofstream(dead) << R"j({"seed":1,"trials":2,"integrands":[{"name":"d","expr":"sqrt(-1-x1)",
        "dim":1,"low":[0],"high":[1],"samples":100}]})j";
   CHECK(run_command(dead, out, {}) == 3);
+  // a tree job (ref tests/test_job_io.cpp:26-50 method round trip), run on the GPU
+  const fs::path tree = dir / "tree_job.json";
+  std::ofstream(tree) << R"j({"seed":31,"trials":2,"integrands":[{"name":"peak",
+       "expr":"exp(-100*((x1-0.3)^2+(x2-0.3)^2))","dim":2,"low":[0,0],"high":[1,1],"samples":1200,
+       "method":"tree","method_config":{"cells_per_dim":2,"samples_per_cell":256}}]})j";
+  CHECK(run_command(tree, out, {}) == 0);
+  auto trows = read_results(out);
+  CHECK(trows.size() == 1 && trows[0].method == "tree" && trows[0].ok);
+  CHECK(trows[0].warnings == "budget_exhausted");
 }
 
 int main(int argc, char** argv) {

@@ -319,8 +319,97 @@ static void fig1_band() {
   CHECK(passed >= 95);
 }
 
+// tests/test_estimator.cpp:140-192 — tree_refine
+static void tree_cases() {
+  auto prog = [](std::string src, std::size_t dim) {
+    return IntegrandSpec::from_source("t", src, dim, HyperRect::unit(dim), {}, 100000);
+  };
+  {  // constant integrand needs no refinement
+    RefineConfig cfg;
+    cfg.total_budget = 100000;
+    std::vector<StratumNode> leaves;
+    McEstimate est = tree_refine(prog("5", 2), cfg, StreamKey{1, 0, 0, 0}, &leaves);
+    CHECK(std::fabs(est.value - 5.0) <= 5e-12);
+    CHECK(est.std_error == 0.0);
+    CHECK(!est.budget_exhausted);
+    CHECK(est.n_samples <= cfg.total_budget);
+    CHECK(leaves.size() == 16);
+  }
+  {  // gaussian peak covers the closed form; leaves tile the domain
+    const double truth = 0.03141592653580133;
+    RefineConfig cfg;
+    cfg.total_budget = 100000;
+    std::vector<StratumNode> leaves;
+    McEstimate est =
+        tree_refine(prog("exp(-100*((x1-0.5)^2+(x2-0.5)^2))", 2), cfg, StreamKey{21, 0, 0, 0}, &leaves);
+    CHECK(std::fabs(est.value - truth) <= 3.0 * est.std_error);
+    double vol = 0.0;
+    for (const StratumNode& n : leaves) vol += n.cell.volume();
+    CHECK(std::fabs(vol - 1.0) <= 1e-12);
+    CHECK(est.n_samples <= cfg.total_budget);
+  }
+  {  // budget exhaustion is flagged, not an error
+    RefineConfig cfg;
+    cfg.init_cells_per_dim = 2;
+    cfg.samples_per_cell = 256;
+    cfg.total_budget = 1200;
+    McEstimate est = tree_refine(prog("exp(-100*((x1-0.3)^2+(x2-0.3)^2))", 2), cfg, StreamKey{31, 0, 0, 0});
+    CHECK(est.budget_exhausted);
+    CHECK(std::isfinite(est.value));
+  }
+  {  // agrees with direct_mc on the oscillatory integrand
+    const double k = 150.0 / (2.0 * std::numbers::pi);
+    IntegrandSpec f = harmonic("osc", k, 4, HyperRect::unit(4), 200000);
+    RefineConfig cfg;
+    cfg.total_budget = 200000;
+    McEstimate tree = tree_refine(f, cfg, StreamKey{5, 0, 0, 0});
+    McEstimate direct = direct_mc(f, 200000, StreamKey{5, 0, 1, 0});
+    const double band = 3.0 * std::sqrt(tree.std_error * tree.std_error + direct.std_error * direct.std_error);
+    CHECK(std::fabs(tree.value - direct.value) <= band);
+  }
+  {  // failures throw like the reference
+    RefineConfig cfg;
+    cfg.cell_cap = 3;
+    CHECK_THROWS_AS(tree_refine(prog("exp(x1)", 2), cfg, StreamKey{16, 0, 0, 0}), CellBudgetExceeded);
+    RefineConfig c2;
+    c2.samples_per_cell = 100;
+    c2.total_budget = 10000;
+    CHECK_THROWS_AS(tree_refine(prog("sqrt(-1-x1)", 1), c2, StreamKey{9, 0, 0, 0}), AllSamplesNonFinite);
+  }
+  {  // run_batch Tree branch: budget = n_samples, budget_exhausted reported, devices invariant
+    JobSpec job;
+    job.seed = 3;
+    job.trials = 3;
+    IntegrandSpec t = prog("exp(-100*((x1-0.3)^2+(x2-0.3)^2))", 2);
+    t.name = "peak";
+    t.method = Method::Tree;
+    RefineConfig rc;
+    rc.init_cells_per_dim = 2;
+    rc.samples_per_cell = 256;
+    t.method_config = rc;
+    t.n_samples = 1200;
+    job.integrands.push_back(t);
+    IntegrandSpec h = harmonic("h", 3.0, 2, HyperRect::unit(2), 50000);
+    h.method = Method::Tree;
+    job.integrands.push_back(h);
+    CHECK(validate(job).empty());
+    BatchResult a = run_batch(job);
+    CHECK(a.per_integrand[0].ok && a.per_integrand[0].budget_exhausted);
+    CHECK(a.per_integrand[1].ok);
+    job.devices = {0, 0};
+    BatchResult b = run_batch(job);
+    for (int i = 0; i < 2; ++i)
+      for (int r = 0; r < 3; ++r) {
+        const McEstimate &x = a.per_integrand[i].summary.per_trial[r], &y = b.per_integrand[i].summary.per_trial[r];
+        CHECK(std::memcmp(&x.value, &y.value, 8) == 0 && std::memcmp(&x.std_error, &y.std_error, 8) == 0 &&
+              x.n_samples == y.n_samples && x.budget_exhausted == y.budget_exhausted);
+      }
+  }
+}
+
 int main() {
   constants_are_exact();
+  tree_cases();
   mixed_dimension_batch();
   validate_reports_every_violation();
   device_invariance();

@@ -7,6 +7,7 @@ Every number in golden.json is produced by the reference's own functions:
   sample_uniform   src/sampling.cpp:102-112
   evaluate         src/expr.cpp:520-553 (on the mcb_to_dsl source)
   direct_mc        src/estimator.cpp:75-92
+  tree_refine      src/estimator.cpp:212-318
   run_batch        src/batch.cpp:195-333
   make_harmonic_job / harmonic_closed_form   src/job_io.cpp:336-376
 Doubles are stored as float.hex() strings so comparisons are bit-exact.
@@ -167,6 +168,10 @@ def main():
     # 7. arbitrary DSL programs (the GPU interpreter's parity anchors)
     g["programs"] = make_program_goldens(ref)
 
+    # 8. tree method: tree_refine (src/estimator.cpp:212-318) standalone with
+    # leaves, and run_batch's Tree branch (src/batch.cpp:276-289)
+    g["tree"] = make_tree_goldens(ref)
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(g, fh, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))
@@ -245,6 +250,72 @@ def make_program_goldens(ref):
                     "n_samples": n, "seed": seed, "index": index, "trial": trial, "chunk_base": cb,
                     "values": [H(float(x)) for x in v], "estimate": stats_json(st)})
     return out
+
+
+# (source, dim, params, low, high, budget, seed, index, trial, chunk_base, refine kwargs)
+TREE_CASES = [
+    ("5", 2, {}, [0, 0], [1, 1], 100_000, 1, 0, 0, 0, {}),                       # test_estimator.cpp:140
+    ("exp(-100*((x1-0.5)^2+(x2-0.5)^2))", 2, {}, [0, 0], [1, 1], 100_000, 21, 0, 0, 0, {}),  # :153
+    ("exp(-100*((x1-0.3)^2+(x2-0.3)^2))", 2, {}, [0, 0], [1, 1], 1_200, 31, 0, 0, 0,
+     {"init_cells_per_dim": 2, "samples_per_cell": 256}),                          # :168 budget exhausted
+    ("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, {"k": 150.0 / (2.0 * np.pi)}, [0] * 4, [1] * 4,
+     200_000, 5, 0, 0, 0, {}),                                                     # :180
+    ("exp(-100*((x1-0.5)^2+(x2-0.5)^2))", 2, {}, [0, 0], [1, 1], 100_000, 0, 0, 0, 0,
+     {"samples_per_cell": 512}),                                                   # acceptance.cpp:163
+    ("exp(-100*((x1-0.5)^2+(x2-0.5)^2))", 2, {}, [0, 0], [1, 1], 100_000, 7, 0, 0, 0,
+     {"samples_per_cell": 512}),
+    ("sqrt(x1-0.6) + x2", 2, {}, [0, 0], [1, 1], 50_000, 4, 2, 1, 0, {"samples_per_cell": 512}),  # dead leaves
+    ("sqrt(-1-x1)", 1, {}, [0], [1], 10_000, 9, 0, 0, 0, {"samples_per_cell": 100}),  # all dead
+    ("a*x1*x2 + sin(b*x3)", 3, {"a": 2.5, "b": 9.0}, [0, -1, 0], [1, 1, 2], 80_000, 12, 3, 2, 7,
+     {"sigma_multiplier": -0.5, "samples_per_cell": 300}),                         # eager splitting
+    ("x1^3 - x2", 2, {}, [-1, -1], [1, 1], 60_000, 13, 0, 0, 0, {"max_depth": 0}),  # no refinement
+    ("abs(x1-x2)", 2, {}, [0, 0], [1, 1], 90_000, 14, 0, 0, 0,
+     {"init_cells_per_dim": 3, "max_depth": 2, "samples_per_cell": 1000}),
+    ("exp(x1)", 2, {}, [0, 0], [1, 1], 10_000, 15, 0, 0, 0, {"init_cells_per_dim": 4, "cell_cap": 10}),
+    ("exp(x1)", 2, {}, [0, 0], [1, 1], 10_000, 16, 0, 0, 0, {"cell_cap": 3}),
+    ("1/(x1-0.5)", 1, {}, [0], [1], 40_000, 17, 0, 0, 0, {"samples_per_cell": 70_000}),  # 2-chunk cells
+]
+
+
+def tree_desc(f, kw):
+    return mcb.tree(f, **kw)
+
+
+def make_tree_goldens(ref):
+    out = []
+    for src, dim, params, lo, hi, budget, seed, index, trial, cb, kw in TREE_CASES:
+        prog = mcb.Program(src, dim, list(params))
+        f = tree_desc(prog.integrand(params, low=lo, high=hi, n_samples=budget, index=index), kw)
+        st, leaves = _oracle.ref_tree_refine(src, f, params, seed, trial, cb)
+        out.append({"source": src, "dim": dim, "params": {k: H(float(x)) for k, x in params.items()},
+                    "low": [H(float(x)) for x in lo], "high": [H(float(x)) for x in hi],
+                    "budget": budget, "seed": seed, "index": index, "trial": trial, "chunk_base": cb,
+                    "refine": kw, "estimate": dict(stats_json(st), budget_exhausted=int(st.budget_exhausted),
+                                                    n_leaves=len(leaves), max_depth=int(st.max_depth)),
+                    "leaves": [[[H(l.low[j]) for j in range(dim)], [H(l.high[j]) for j in range(dim)],
+                                int(l.depth), H(l.estimate.value), H(l.estimate.std_error),
+                                int(l.estimate.n_nonfinite)] for l in leaves]})
+    # run_batch Tree branch on family integrands, 3 trials
+    fns = [mcb.tree(mcb.harmonic(150 / (2 * np.pi), 4, unit_coeffs=True, n_samples=100_000, index=0)),
+           mcb.tree(mcb.make_integrand(mcb.FAMILY_ABS3, 3, a=2.0, low=[-1, 0, 0.5], high=[1, 2, 3],
+                                       n_samples=60_000, index=1), samples_per_cell=512, sigma_multiplier=0.5),
+           mcb.tree(mcb.harmonic(3.0, 2, a=0.5, b=-1.5, n_samples=1_200, index=2), init_cells_per_dim=2,
+                    samples_per_cell=256),
+           mcb.tree(mcb.make_integrand(mcb.FAMILY_HARMONIC_VEC, 3, k=[2.0, -1.0, 9.5], a=1.5, b=0.5,
+                                       low=[-1, 0, 0.5], high=[1, 2, 1.5], n_samples=150_000, index=3),
+                    samples_per_cell=1024, max_depth=3),
+           mcb.tree(mcb.make_integrand(mcb.FAMILY_ABS2, 2, n_samples=30_000, index=4), sigma_multiplier=0.0,
+                    samples_per_cell=200)]
+    o, mean, sd, ok, _ = _oracle.ref_run_batch(fns, 77, 3, workers=0)
+    batch = [{"desc": desc_json(f), "refine": {"init_cells_per_dim": int(f.cells_per_dim),
+                                                "samples_per_cell": int(f.samples_per_cell),
+                                                "max_depth": int(f.max_depth),
+                                                "sigma_multiplier": H(f.sigma_multiplier)},
+              "per_trial": [dict(stats_json(_as_stats(o[i, t])), budget_exhausted=int(o[i, t]["budget_exhausted"]))
+                            for t in range(3)],
+              "mean": H(float(mean[i])), "trial_stddev": H(float(sd[i])), "ok": int(ok[i])}
+             for i, f in enumerate(fns)]
+    return {"cases": out, "batch": {"seed": 77, "trials": 3, "cases": batch}}
 
 
 def _as_stats(row):

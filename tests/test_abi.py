@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(mcb):
     out = os.popen(f"nm -D --defined-only {mcb.LIB_PATH}").read()
     exported = set(re.findall(r" T (mcb_\w+)", out))
     assert set(decl) <= exported, set(decl) - exported
-    assert mcb.lib.mcb_abi_version() == 1
+    assert mcb.lib.mcb_abi_version() == 2
 
 
 def test_library_is_native_sm100a(mcb):
