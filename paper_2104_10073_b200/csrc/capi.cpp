@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -308,8 +309,11 @@ struct Prepared {
 // |t| < 2^20 for the table reduction, no overflow of f, and exact 2^-64
 // folding.  Anything else runs the SAFE variant (libdevice sincos, counted
 // non-finite samples) — still on the GPU.
+// tree_cells: the descriptor of one tree's cells in a refinement round (the
+// caller sets n_cells / spc / cpc / cell_rects / cell_est); cells are at
+// least width / (k0 * 2^depth) wide, which bounds the 2^-64 fold.
 Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
-                 uint32_t trial_base) {
+                 uint32_t trial_base, bool tree_cells = false) {
   using namespace mcb::detail;
   Prepared p;
   FnDesc& d = p.d;
@@ -320,9 +324,14 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   d.key1 = key[1];
   d.n_chunks = uint32_t(chunk_count(f.n_samples));
   d.dim = f.dim;
-  const bool strat = stratified(f);
+  const bool strat = stratified(f) || tree_cells;
   double cell_k = 1.0;
-  if (strat) {  // tiles per trial = cells x chunks per cell
+  if (tree_cells) {
+    const mcb::tree::Config rc = mcb::tree::config_of(f);
+    const uint32_t k0 = rc.init_cells_per_dim ? rc.init_cells_per_dim : auto_cells_per_dim(f.dim, 4096);
+    const uint64_t splits = f.n_samples / (2ull * std::max<uint32_t>(rc.samples_per_cell, 2)) + 1;
+    cell_k = double(k0) * std::ldexp(1.0, int(std::min<uint64_t>({uint64_t(rc.max_depth), splits, 2000ull})));
+  } else if (strat) {  // tiles per trial = cells x chunks per cell
     const StratPlan sp = stratified_plan(f);
     d.strat_k = sp.k;
     d.n_cells = uint32_t(sp.n_cells);
@@ -384,7 +393,10 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
       else fast = foldable(f.a);
     } else {
       // cells are >= width/k wide (the device folds each cell's width)
-      for (uint32_t j = 0; j < f.dim; ++j) fast = fast && foldable(0.5 * d.width[j] / cell_k);
+      for (uint32_t j = 0; j < f.dim; ++j) {
+        const double w = 0.5 * d.width[j] / cell_k;
+        fast = fast && w >= kMinFold && std::isfinite(w);
+      }
     }
   }
   if (fast) {
@@ -412,6 +424,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   }
   if (!harm) p.variant &= ~kUnitCoef;
   if (strat) p.variant |= kStrat;
+  if (tree_cells) p.variant &= ~kNoShift;  // cells shrink: keep the per-tile shift
   // shift constant: f at the domain midpoint (reference op order, libm)
   double mid[MCB_MAX_DIM];
   for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
@@ -580,7 +593,10 @@ struct DevBuf {
   mcb_trial_stats* out = nullptr;
   uint32_t* code = nullptr;
   double* consts = nullptr;
+  double* rects = nullptr;              // tree rounds: cell rectangles
+  mcb_trial_stats* cell_est = nullptr;  //   and per-cell estimates
   size_t cap_fns = 0, cap_tiles = 0, cap_part = 0, cap_out = 0, cap_code = 0, cap_consts = 0;
+  size_t cap_rects = 0, cap_cell_est = 0;
 
   template <class T>
   static cudaError_t grow(T*& p, size_t& cap, size_t need) {
@@ -610,6 +626,8 @@ struct DevBuf {
     if (out) cudaFree(out);
     if (code) cudaFree(code);
     if (consts) cudaFree(consts);
+    if (rects) cudaFree(rects);
+    if (cell_est) cudaFree(cell_est);
     *this = DevBuf{};
   }
 };
@@ -656,6 +674,10 @@ struct DeviceCtx {
   size_t h_descs_cap = 0;
   mcb_trial_stats* h_out = nullptr;
   size_t h_out_cap = 0;
+  double* h_rects = nullptr;
+  size_t h_rects_cap = 0;
+  mcb_trial_stats* h_cell_est = nullptr;
+  size_t h_cell_est_cap = 0;
 };
 
 DeviceCtx& device_ctx(int device) {
@@ -684,8 +706,17 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
                      int device, mcb_trial_stats* out, const uint32_t* chunk_bases = nullptr,
                      const uint32_t* trial_bases = nullptr) {
   HostPlan hp;
+  const auto tb0 = std::chrono::steady_clock::now();
   mcb_status st = build_host_plan(fns, n_fns, seed, trials, 0, 0, hp, chunk_bases, trial_bases);
   if (st != MCB_OK) return st;
+  static const bool trace = [] {
+    const char* e = std::getenv("MCB_TREE_TRACE");
+    return e && *e && *e != '0';
+  }();
+  if (trace)
+    std::fprintf(stderr, "[mcb shard] dev %d: %zu fns, %llu tiles, host plan %.3f ms\n", device, n_fns,
+                 (unsigned long long)hp.n_tiles,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb0).count());
   DeviceCtx& c = device_ctx(device);
   std::lock_guard<std::mutex> lock(c.mu);
   DeviceGuard guard(device);
@@ -707,6 +738,117 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
     return cuda_fail(e, "cudaMemcpyAsync(results)");
   if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   std::memcpy(out, c.h_out, sizeof(mcb_trial_stats) * n_out);
+  return MCB_OK;
+}
+
+// One device's share of a tree round: a cell-list descriptor per batch
+// (prepared as the tree's integrand, cells from the rectangle table), the
+// fused kernels in cell-list mode, per-cell estimates back to the batches.
+mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batches, uint64_t seed,
+                          int device) {
+  const size_t n = batches.size();
+  HostPlan hp;
+  std::vector<Prepared> prep(n);
+  size_t n_rects = 0, n_cells = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const mcb::tree::CellBatch& b = *batches[i];
+    prep[i] = prepare(*b.fn, seed, uint32_t(b.chunk_base), b.trial, true);
+    n_rects += size_t(b.n_cells) * 2 * b.fn->dim;
+    n_cells += b.n_cells;
+  }
+  std::vector<size_t> order(n);
+  std::iota(order.begin(), order.end(), size_t(0));
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+    return std::make_tuple(batches[x]->fn->family, batches[x]->fn->dim, prep[x].variant) <
+           std::make_tuple(batches[y]->fn->family, batches[y]->fn->dim, prep[y].variant);
+  });
+  uint64_t tiles = 0;
+  for (size_t i = 0; i < n; ++i) tiles += uint64_t(batches[i]->n_cells) * chunk_count(batches[i]->spc);
+
+  DeviceCtx& c = device_ctx(device);
+  std::lock_guard<std::mutex> lock(c.mu);
+  DeviceGuard guard(device);
+  cudaError_t e;
+  if (!c.ready) {
+    if ((e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+    c.ready = true;
+  }
+  // program tables first (sizes), then buffers, then descriptors with device addresses
+  std::map<const mcb_program*, std::pair<uint32_t, uint32_t>> prog_at;
+  for (size_t i = 0; i < n; ++i) {
+    const mcb_program* pg = batches[i]->fn->program;
+    if (batches[i]->fn->family != MCB_FAMILY_PROGRAM || prog_at.count(pg)) continue;
+    prog_at.emplace(pg, std::make_pair(uint32_t(hp.code.size()), uint32_t(hp.consts.size())));
+    hp.code.insert(hp.code.end(), pg->words.begin(), pg->words.end());
+    hp.consts.insert(hp.consts.end(), pg->p.consts.begin(), pg->p.consts.end());
+  }
+  if ((e = c.buf.reserve(n, tiles, n, hp.code.size(), hp.consts.size())) != cudaSuccess ||
+      (e = DevBuf::grow(c.buf.rects, c.buf.cap_rects, n_rects)) != cudaSuccess ||
+      (e = DevBuf::grow(c.buf.cell_est, c.buf.cap_cell_est, n_cells)) != cudaSuccess)
+    return cuda_fail(e, "cudaMalloc");
+  if ((e = grow_pinned(c.h_descs, c.h_descs_cap, n)) != cudaSuccess ||
+      (e = grow_pinned(c.h_rects, c.h_rects_cap, n_rects)) != cudaSuccess ||
+      (e = grow_pinned(c.h_cell_est, c.h_cell_est_cap, n_cells)) != cudaSuccess)
+    return cuda_fail(e, "cudaMallocHost");
+  hp.descs.resize(n);
+  std::vector<size_t> est_at(n);
+  uint64_t tile = 0;
+  size_t rect_at = 0, cell_at = 0;
+  for (size_t r = 0; r < n; ++r) {
+    const size_t i = order[r];
+    const mcb::tree::CellBatch& b = *batches[i];
+    FnDesc d = prep[i].d;
+    d.strat_k = 0;
+    d.n_cells = b.n_cells;
+    d.spc = b.spc;
+    d.cpc = uint32_t(chunk_count(b.spc));
+    d.n_chunks = d.n_cells * d.cpc;
+    d.n_samples = uint64_t(b.n_cells) * b.spc;
+    d.tile_base = tile;
+    d.out_slot = r;
+    d.cell_rects = c.buf.rects + rect_at;
+    d.cell_est = c.buf.cell_est + cell_at;
+    const size_t nr = size_t(b.n_cells) * 2 * b.fn->dim;
+    std::memcpy(c.h_rects + rect_at, b.rects, sizeof(double) * nr);
+    est_at[i] = cell_at;
+    rect_at += nr;
+    cell_at += b.n_cells;
+    const int fam = int(b.fn->family), dim = int(b.fn->dim), var = prep[i].variant;
+    uint32_t slots = 0;
+    if (fam == MCB_FAMILY_PROGRAM) {
+      const auto& at = prog_at.at(b.fn->program);
+      d.prog_off = at.first;
+      d.prog_len = uint32_t(b.fn->program->p.code.size());
+      d.const_off = at.second;
+      d.n_consts = uint32_t(b.fn->program->p.consts.size());
+      slots = b.fn->program->p.depth;
+    }
+    if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
+        hp.groups.back().variant != var)
+      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0});
+    hp.groups.back().n_tiles += d.n_chunks;
+    hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
+    tile += d.n_chunks;
+    hp.descs[r] = d;
+  }
+  hp.n_tiles = tile;
+  for (const auto& g : hp.groups)
+    if (g.family != MCB_FAMILY_PROGRAM && !mcb::detail::variant_supported(g.family, g.dim, g.variant))
+      return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
+  std::memcpy(c.h_descs, hp.descs.data(), sizeof(FnDesc) * n);
+  if (n_rects &&
+      (e = cudaMemcpyAsync(c.buf.rects, c.h_rects, sizeof(double) * n_rects, cudaMemcpyHostToDevice,
+                           c.stream)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync(cells)");
+  mcb_status st = enqueue_run(hp, c.buf, 1, c.h_descs, true, c.stream);
+  if (st != MCB_OK) return st;
+  if ((e = cudaMemcpyAsync(c.h_cell_est, c.buf.cell_est, sizeof(mcb_trial_stats) * n_cells,
+                           cudaMemcpyDeviceToHost, c.stream)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync(cell estimates)");
+  if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  for (size_t i = 0; i < n; ++i)
+    std::memcpy(batches[i]->est, c.h_cell_est + est_at[i], sizeof(mcb_trial_stats) * batches[i]->n_cells);
   return MCB_OK;
 }
 
@@ -842,17 +984,46 @@ mcb_status run_sharded(const mcb_integrand* fns, size_t n_fns, uint64_t seed, ui
   return MCB_OK;
 }
 
-// One round of tree cells: 1-trial direct units with per-cell key bases.
-mcb_status run_cells(const std::vector<mcb::tree::CellJob>& jobs, uint64_t seed, const std::vector<int>& devs,
-                     mcb_trial_stats* out) {
-  std::vector<mcb_integrand> fns(jobs.size());
-  std::vector<uint32_t> cb(jobs.size()), tb(jobs.size());
-  for (size_t i = 0; i < jobs.size(); ++i) {
-    fns[i] = jobs[i].fn;
-    cb[i] = uint32_t(jobs[i].chunk_base);  // < 2^32: checked by the driver
-    tb[i] = jobs[i].trial;
+// One tree round: batches sharded over `devs` by LPT on their sample cost.
+mcb_status run_cells(const std::vector<mcb::tree::CellBatch>& batches, uint64_t seed,
+                     const std::vector<int>& devs) {
+  const size_t n = batches.size();
+  std::vector<std::vector<const mcb::tree::CellBatch*>> shard(devs.size());
+  if (devs.size() == 1) {
+    for (const auto& b : batches) shard[0].push_back(&b);
+  } else {
+    std::vector<size_t> order(n);
+    std::iota(order.begin(), order.end(), size_t(0));
+    std::vector<double> cost(n);
+    for (size_t i = 0; i < n; ++i)
+      cost[i] = double(batches[i].n_cells) * double(batches[i].spc) * sample_cost(*batches[i].fn);
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
+    std::vector<double> load(devs.size(), 0.0);
+    for (size_t i : order) {
+      size_t best = 0;
+      for (size_t w = 1; w < load.size(); ++w)
+        if (load[w] < load[best]) best = w;
+      shard[best].push_back(&batches[i]);
+      load[best] += cost[i];
+    }
   }
-  return run_sharded(fns.data(), fns.size(), seed, 1, devs, out, cb.data(), tb.data());
+  std::vector<mcb_status> status(devs.size(), MCB_OK);
+  std::vector<std::string> errors(devs.size());
+  auto work = [&](size_t w) {
+    if (shard[w].empty()) return;
+    status[w] = run_cell_shard(shard[w], seed, devs[w]);
+    if (status[w] != MCB_OK) errors[w] = g_last_error;
+  };
+  if (devs.size() == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (size_t w = 0; w < devs.size(); ++w) pool.emplace_back(work, w);
+    for (auto& th : pool) th.join();
+  }
+  for (size_t w = 0; w < devs.size(); ++w)
+    if (status[w] != MCB_OK) return fail(status[w], "device " + std::to_string(devs[w]) + ": " + errors[w]);
+  return MCB_OK;
 }
 
 }  // namespace
@@ -1040,9 +1211,9 @@ mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
     for (size_t i : trees)
       for (uint32_t t = 0; t < trials; ++t)
         tasks.push_back(mcb::tree::TreeTask{&fns[i], t, 0, out + i * trials + t, nullptr});
-    if ((st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellJob>& jobs,
-                                              mcb_trial_stats* o) { return run_cells(jobs, seed, devs, o); })) !=
-        MCB_OK)
+    if ((st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
+           return run_cells(batches, seed, devs);
+         })) != MCB_OK)
       return st;
   }
   const auto t1 = std::chrono::steady_clock::now();
@@ -1065,8 +1236,8 @@ mcb_status mcb_tree_refine(const mcb_integrand* fn, uint64_t seed, uint32_t tria
   std::vector<mcb_leaf> lv;
   std::vector<mcb::tree::TreeTask> tasks{mcb::tree::TreeTask{&f, trial, chunk_base, out, &lv}};
   const std::vector<int> devs{device};
-  st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellJob>& jobs, mcb_trial_stats* o) {
-    return run_cells(jobs, seed, devs, o);
+  st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
+    return run_cells(batches, seed, devs);
   });
   if (st != MCB_OK) return st;
   if (n_leaves) *n_leaves = lv.size();

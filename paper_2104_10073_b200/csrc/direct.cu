@@ -51,6 +51,14 @@ __device__ double cell_volume(const FnDesc& F, uint32_t cell) {
   return v;
 }
 
+// HyperRect::volume of a listed cell (tree round), left to right from 1.0.
+__device__ double rect_volume(const FnDesc& F, uint32_t cell) {
+  const double* r = F.cell_rects + uint64_t(cell) * (2 * F.dim);
+  double v = 1.0;
+  for (uint32_t j = 0; j < F.dim; ++j) v = __dmul_rn(v, __dsub_rn(r[F.dim + j], r[j]));
+  return v;
+}
+
 struct Accum {  // ChunkAccum (ref src/estimator.cpp:9-34): n, n_nonfinite, mean, m2
   uint64_t n = 0, nn = 0;
   double mean = 0.0, m2 = 0.0;
@@ -97,7 +105,7 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
   st.n_cells = 1;
   st.budget_exhausted = 0;
   st.max_depth = 0;
-  if (F.strat_k > 0) {
+  if (F.strat_k > 0 || F.cell_rects) {
     double value = 0.0, var = 0.0;
     uint64_t n_all = 0, nn_all = 0;
     int dead = -1;
@@ -106,11 +114,29 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
       for (uint32_t cc = 0; cc < F.cpc; ++cc) merge_tile(a, part[base + uint64_t(c) * F.cpc + cc]);
       n_all += a.n + a.nn;
       nn_all += a.nn;
+      const double vol = F.cell_rects ? rect_volume(F, c) : cell_volume(F, c);
+      if (F.cell_est) {  // tree round: each cell's own direct_mc estimate (reduce_chunks)
+        mcb_trial_stats cs;
+        cs.n_samples = a.n + a.nn;
+        cs.n_nonfinite = a.nn;
+        cs.status = a.n == 0 ? MCB_TRIAL_ALL_NONFINITE : MCB_TRIAL_OK;
+        cs.nonfinite_warning = double(a.nn) > MCB_NONFINITE_WARN_FRACTION * double(a.n + a.nn) ? 1u : 0u;
+        cs.detail = 0;
+        cs.n_cells = 1;
+        cs.budget_exhausted = 0;
+        cs.max_depth = 0;
+        cs.value = a.n == 0 ? 0.0 : __dmul_rn(vol, a.mean);
+        cs.std_error = a.n == 0 ? 0.0
+                       : a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)),
+                                                                          double(a.n))))
+                                  : __longlong_as_double(0x7FF0000000000000ll);
+        F.cell_est[c] = cs;
+        continue;
+      }
       if (a.n == 0) {
         if (dead < 0) dead = int(c);
         continue;
       }
-      const double vol = cell_volume(F, c);
       value = __dadd_rn(value, __dmul_rn(vol, a.mean));
       const double se = a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)),
                                                                          double(a.n))))

@@ -65,10 +65,11 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
   uint32_t count;
   if (STRAT) {
     // stratified_mc cell `cell`: direct_mc over grid_cell(domain, k, cell) with
-    // spc samples and chunk keys cell * cpc + c (ref src/batch.cpp:255-275)
+    // spc samples and chunk keys cell * cpc + c (ref src/batch.cpp:255-275);
+    // a tree round's listed cell likewise (ref src/estimator.cpp:238-253)
     const uint32_t cell = chunk / f.cpc, cc = chunk - cell * f.cpc;
     count = (cc + 1 == f.cpc) ? f.spc - cc * MCB_CHUNK_SIZE : MCB_CHUNK_SIZE;
-    dev::grid_cell<D>(f, f.strat_k, cell, SAFE ? 1.0 : dev::kTwoM64);
+    dev::cell_rect<D>(f, cell, SAFE ? 1.0 : dev::kTwoM64);
   } else {
     count = (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
                                       : MCB_CHUNK_SIZE;

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
   if (STRAT) {  // see k_direct: cells of stratified_mc (ref src/batch.cpp:255-275)
     const uint32_t cell = chunk / f.cpc, cc = chunk - cell * f.cpc;
     count = (cc + 1 == f.cpc) ? f.spc - cc * MCB_CHUNK_SIZE : MCB_CHUNK_SIZE;
-    dev::grid_cell<D>(f, f.strat_k, cell, 1.0);
+    dev::cell_rect<D>(f, cell, 1.0);
   } else {
     count = (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
                                       : MCB_CHUNK_SIZE;

@@ -7,7 +7,10 @@
 #include "tree.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace mcb::tree {
@@ -59,36 +62,29 @@ struct Tree {
   bool exhausted = false;
   bool active = true;
   uint32_t fail = MCB_TRIAL_OK;  // CELL_BUDGET / CHUNK_RANGE: the tree threw
-};
-
-// The per-round batch: jobs plus the (tree, leaf) each result lands in.
-struct Round {
-  std::vector<CellJob> jobs;
-  std::vector<std::pair<Tree*, size_t>> dest;
+  // this round's cells: leaf index, rectangle, estimate; chunk of the first
+  std::vector<size_t> r_leaf;
+  std::vector<double> r_rects;
+  std::vector<mcb_trial_stats> r_est;
+  uint64_t r_chunk0 = 0;
 };
 
 // estimate_cell (src/estimator.cpp:238-253): key chunk next_chunk, then
-// next_chunk += chunks_per_cell and used += spc.
-void estimate_cell(Tree& t, size_t leaf, Round& r) {
+// next_chunk += chunks_per_cell and used += spc.  The estimate is deferred
+// to the round's launch.
+void estimate_cell(Tree& t, size_t leaf) {
   if (t.next_chunk + t.cpc - 1 > 0xFFFFFFFFull) {  // UniformStream throws (src/sampling.cpp:80-81)
     t.fail = MCB_TRIAL_CHUNK_RANGE;
     t.active = false;
     return;
   }
-  CellJob j;
-  j.fn = *t.task->fn;
-  j.fn.method = MCB_METHOD_DIRECT;
-  j.fn.flags &= ~MCB_FLAG_REFINE_CONFIG;
-  j.fn.cells_per_dim = 0;
-  j.fn.n_samples = t.spc;
-  std::memcpy(j.fn.low, t.leaves[leaf].low, sizeof j.fn.low);
-  std::memcpy(j.fn.high, t.leaves[leaf].high, sizeof j.fn.high);
-  j.chunk_base = t.next_chunk;
-  j.trial = t.task->trial;
+  if (t.r_leaf.empty()) t.r_chunk0 = t.next_chunk;
+  t.r_leaf.push_back(leaf);
+  const Leaf& l = t.leaves[leaf];
+  t.r_rects.insert(t.r_rects.end(), l.low, l.low + t.dim);
+  t.r_rects.insert(t.r_rects.end(), l.high, l.high + t.dim);
   t.next_chunk += t.cpc;
   t.used += t.spc;
-  r.jobs.push_back(j);
-  r.dest.emplace_back(&t, leaf);
 }
 
 // The AllSamplesNonFinite catch of estimate_cell: a dead leaf.
@@ -102,26 +98,56 @@ mcb_trial_stats dead_leaf(uint32_t spc) {
   return s;
 }
 
-mcb_status run_round(Round& r, const CellRunner& run) {
-  if (r.jobs.empty()) return MCB_OK;
-  std::vector<mcb_trial_stats> res(r.jobs.size());
-  const mcb_status st = run(r.jobs, res.data());
-  if (st != MCB_OK) return st;
-  for (size_t i = 0; i < r.jobs.size(); ++i) {
-    Tree& t = *r.dest[i].first;
-    if (t.fail != MCB_TRIAL_OK) continue;
-    mcb_trial_stats& e = t.leaves[r.dest[i].second].est;
-    if (res[i].status == MCB_TRIAL_OK) {
-      e = res[i];
-      e.n_cells = 1;
-      e.budget_exhausted = 0;
-      e.max_depth = 0;
-    } else {
-      e = dead_leaf(t.spc);
+// MCB_TREE_TRACE=1: per-round cell counts and times on stderr.
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MCB_TREE_TRACE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
+// One launch set for every tree's pending cells, then the results land in
+// the leaves.
+mcb_status run_round(std::vector<Tree>& trees, const CellRunner& run) {
+  std::vector<CellBatch> batches;
+  std::vector<Tree*> owner;
+  size_t cells = 0;
+  for (Tree& t : trees) {
+    if (t.r_leaf.empty()) continue;
+    if (t.fail != MCB_TRIAL_OK) {
+      t.r_leaf.clear();
+      t.r_rects.clear();
+      continue;
     }
+    t.r_est.assign(t.r_leaf.size(), mcb_trial_stats{});
+    batches.push_back(CellBatch{t.task->fn, t.task->trial, t.r_chunk0, t.spc, uint32_t(t.r_leaf.size()),
+                                t.r_rects.data(), t.r_est.data()});
+    owner.push_back(&t);
+    cells += t.r_leaf.size();
   }
-  r.jobs.clear();
-  r.dest.clear();
+  if (batches.empty()) return MCB_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  const mcb_status st = run(batches);
+  if (trace_on())
+    std::fprintf(stderr, "[mcb tree] round: %zu trees, %zu cells, %.3f ms\n", batches.size(), cells,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  if (st != MCB_OK) return st;
+  for (Tree* t : owner) {
+    for (size_t i = 0; i < t->r_leaf.size(); ++i) {
+      mcb_trial_stats& e = t->leaves[t->r_leaf[i]].est;
+      if (t->r_est[i].status == MCB_TRIAL_OK) {
+        e = t->r_est[i];
+        e.n_cells = 1;
+        e.budget_exhausted = 0;
+        e.max_depth = 0;
+      } else {
+        e = dead_leaf(t->spc);
+      }
+    }
+    t->r_leaf.clear();
+    t->r_rects.clear();
+  }
   return MCB_OK;
 }
 
@@ -144,7 +170,7 @@ void split_longest_edge(const Leaf& cell, uint32_t d, Leaf& lo, Leaf& hi) {
 }
 
 // One refinement step of the `while (!exhausted)` loop, src/estimator.cpp:265-297.
-void refine_step(Tree& t, Round& r) {
+void refine_step(Tree& t) {
   const size_t n = t.leaves.size();
   double mean_err = 0.0;
   for (const Leaf& l : t.leaves) mean_err += l.est.std_error;
@@ -177,9 +203,9 @@ void refine_step(Tree& t, Round& r) {
     t.leaves[idx] = lo;  // the lower half replaces the parent in place
     t.leaves.push_back(hi);
     const size_t hi_idx = t.leaves.size() - 1;
-    estimate_cell(t, idx, r);
+    estimate_cell(t, idx);
     if (t.fail != MCB_TRIAL_OK) return;
-    estimate_cell(t, hi_idx, r);
+    estimate_cell(t, hi_idx);
     if (t.fail != MCB_TRIAL_OK) return;
   }
   if (t.exhausted) t.active = false;  // the while condition
@@ -250,7 +276,6 @@ Config config_of(const mcb_integrand& f) {
 
 mcb_status run_trees(std::vector<TreeTask>& tasks, const CellRunner& run) {
   std::vector<Tree> trees(tasks.size());
-  Round r;
   // First pass (src/estimator.cpp:215-263): grid size, then every grid cell.
   for (size_t i = 0; i < tasks.size(); ++i) {
     Tree& t = trees[i];
@@ -295,19 +320,21 @@ mcb_status run_trees(std::vector<TreeTask>& tasks, const CellRunner& run) {
         l.high[j] = digit + 1 == k ? f.high[j] : f.low[j] + width * (double(digit + 1) / k);
       }
     }
-    for (uint64_t c = 0; c < n_cells && t.fail == MCB_TRIAL_OK; ++c) estimate_cell(t, c, r);
+    t.r_leaf.reserve(n_cells);
+    t.r_rects.reserve(n_cells * 2 * t.dim);
+    for (uint64_t c = 0; c < n_cells && t.fail == MCB_TRIAL_OK; ++c) estimate_cell(t, c);
   }
-  mcb_status st = run_round(r, run);
+  mcb_status st = run_round(trees, run);
   if (st != MCB_OK) return st;
   for (;;) {
     bool any = false;
     for (Tree& t : trees)
       if (t.active) {
-        refine_step(t, r);
+        refine_step(t);
         any = true;
       }
     if (!any) break;
-    if ((st = run_round(r, run)) != MCB_OK) return st;
+    if ((st = run_round(trees, run)) != MCB_OK) return st;
   }
   for (Tree& t : trees) finish(t);
   return MCB_OK;

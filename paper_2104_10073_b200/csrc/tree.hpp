@@ -7,9 +7,9 @@
 // is independent, and so is every tree of a batch.  The driver therefore runs
 // all trees in lock-step rounds: round 0 estimates every tree's initial grid,
 // round r every cell split in round r; each round's cells of ALL trees go to
-// the GPU as one batch of 1-trial direct_mc units (CellJob) through
-// `CellRunner`, which the C-ABI layer (capi.cpp) implements with the fused
-// direct kernels sharded over the devices.  Selection, splitting and budget
+// the GPU as one launch set through `CellRunner`: per tree a cell-list
+// descriptor + its cell rectangles, estimated by the fused kernels in
+// cell-list mode and sharded over the devices (capi.cpp).  Selection, splitting and budget
 // accounting repeat the reference's host arithmetic operation for operation.
 #pragma once
 
@@ -22,18 +22,23 @@
 
 namespace mcb::tree {
 
-// One direct_mc unit: `fn` restricted to a cell (low/high = the cell,
-// n_samples = samples per cell, method DIRECT) with key base
-// {seed, fn.integrand_index, trial, chunk_base}.
-struct CellJob {
-  mcb_integrand fn;
-  uint64_t chunk_base;
+// One tree's new cells of a refinement round: cell c is a direct_mc unit of
+// `fn` restricted to rects[c] with spc samples and key base
+// {seed, fn->integrand_index, trial, chunk_base + c * chunk_count(spc)}
+// (consecutive estimate_cell calls, ref src/estimator.cpp:238-253).
+struct CellBatch {
+  const mcb_integrand* fn;  // method TREE
   uint32_t trial;
+  uint64_t chunk_base;
+  uint32_t spc;
+  uint32_t n_cells;
+  const double* rects;      // n_cells x {low[dim], high[dim]}
+  mcb_trial_stats* est;     // n_cells per-cell estimates (status ALL_NONFINITE = no finite sample)
 };
 
-// Estimates `jobs` (results in job order).  Returns MCB_OK or an error status
+// Estimates every batch of a round.  Returns MCB_OK or an error status
 // (message already recorded by the implementation).
-using CellRunner = std::function<mcb_status(const std::vector<CellJob>& jobs, mcb_trial_stats* out)>;
+using CellRunner = std::function<mcb_status(const std::vector<CellBatch>& batches)>;
 
 struct TreeTask {
   const mcb_integrand* fn;   // method TREE; n_samples = total_budget

@@ -57,6 +57,12 @@ def rel_close(got, want, tol=1e-12, scale=0.0):
     return abs(got - want) <= tol * max(abs(want), scale)
 
 
+def est_close(got, want, se):
+    """Estimates agree to rounding: 1e-12 relative, or 1e-9 of the statistical
+    error (a cell mean of an oscillating integrand cancels far below |f|)."""
+    return abs(got - want) <= 1e-12 * abs(want) + 1e-9 * se
+
+
 # ---------------------------------------------------------------- CPU
 
 
@@ -151,14 +157,13 @@ def test_tree_vs_reference_golden(gpu, tg):
         assert st.n_samples == want["n_samples"] and st.n_nonfinite == want["n_nonfinite"]
         assert st.budget_exhausted == want["budget_exhausted"] and st.max_depth == want["max_depth"]
         assert st.nonfinite_warning == want["nonfinite_warning"]
-        scale = max(abs(fx(lw[3])) for lw in c["leaves"])
         for got, (lo, hi, depth, val, se, nn) in zip(leaves, c["leaves"]):
             assert [got.low[j] for j in range(c["dim"])] == [fx(x) for x in lo]
             assert [got.high[j] for j in range(c["dim"])] == [fx(x) for x in hi]
             assert got.depth == depth and got.estimate.n_nonfinite == nn
-            assert rel_close(got.estimate.value, fx(val), 1e-12, 1e-3 * scale), c["source"]
+            assert est_close(got.estimate.value, fx(val), fx(se)), c["source"]
             assert rel_close(got.estimate.std_error, fx(se), 1e-9), c["source"]
-        assert rel_close(st.value, fx(want["value"]), 1e-12, 1e-3 * scale)
+        assert est_close(st.value, fx(want["value"]), fx(want["std_error"]))
         assert rel_close(st.std_error, fx(want["std_error"]), 1e-9)
 
 
@@ -173,10 +178,10 @@ def test_tree_batch_vs_reference_golden(gpu, tg):
             assert int(got["status"]) == gpu.TRIAL_OK
             assert int(got["n_samples"]) == want["n_samples"], (i, t)
             assert int(got["budget_exhausted"]) == want["budget_exhausted"], (i, t)
-            assert rel_close(float(got["value"]), fx(want["value"]), 1e-11, 1e-6), (i, t)
+            assert est_close(float(got["value"]), fx(want["value"]), fx(want["std_error"])), (i, t)
             assert rel_close(float(got["std_error"]), fx(want["std_error"]), 1e-9), (i, t)
         mean, sd, n_ok = gpu.summarize_trials(out[i])
-        assert rel_close(mean, fx(c["mean"]), 1e-11, 1e-6)
+        assert est_close(mean, fx(c["mean"]), fx(c["per_trial"][0]["std_error"]))
 
 
 @pytest.mark.gpu
@@ -204,8 +209,7 @@ def test_tree_vs_oracle_random_families(gpu, oracle):
             assert list(a.low) == list(b.low) and list(a.high) == list(b.high) and a.depth == b.depth
         assert (sg.n_samples, sg.budget_exhausted, sg.max_depth) == (so.n_samples, so.budget_exhausted,
                                                                      so.max_depth)
-        scale = abs(f.a) + abs(f.b)
-        assert rel_close(sg.value, so.value, 1e-11, 1e-4 * scale * gpu.volume(f)), it
+        assert est_close(sg.value, so.value, so.std_error), it
         assert rel_close(sg.std_error, so.std_error, 1e-9), it
 
 
