@@ -203,15 +203,17 @@ def load_ref():
     return lib
 
 
-def ref_run_batch(fns, seed, trials, workers=0):
-    """run_batch of the unmodified reference on the lowered DSL sources."""
+def ref_run_batch(fns, seed, trials, workers=0, sources=None):
+    """run_batch of the unmodified reference on the lowered DSL sources (or
+    `sources`: parameter-free DSL per integrand, for PROGRAM descriptors)."""
     from paper_2104_10073_b200 import TRIAL_DTYPE, as_array, to_dsl
     lib = load_ref()
     if lib is None:
         raise FileNotFoundError(REF_SO)
     arr = as_array(fns)
     n = len(arr)
-    srcs = (ctypes.c_char_p * n)(*[to_dsl(arr[i]).encode() for i in range(n)])
+    texts = sources if sources is not None else [to_dsl(arr[i]) for i in range(n)]
+    srcs = (ctypes.c_char_p * n)(*[t.encode() for t in texts])
     out = np.zeros((n, trials), dtype=TRIAL_DTYPE)
     mean = np.zeros(n)
     sd = np.zeros(n)

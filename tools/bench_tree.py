@@ -25,15 +25,25 @@ def main():
     ap.add_argument("--spc", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--ref-fns", type=int, default=8)
+    ap.add_argument("--integrand", choices=["harmonic", "peak"], default="harmonic",
+                    help="harmonic: Fig.1 family (4-D); peak: the C5 gaussian peak DSL program (2-D)")
     args = ap.parse_args()
     import numpy as np
 
     import paper_2104_10073_b200 as mcb
     from paper_2104_10073_b200 import workloads as w
 
-    fns = [mcb.tree(mcb.harmonic(w.harmonic_k(n), 4, unit_coeffs=True, n_samples=args.budget, index=i),
-                    samples_per_cell=args.spc)
-           for i, n in enumerate(list(range(1, 101)) * ((args.fns + 99) // 100))][:args.fns]
+    keep, sources = None, None
+    if args.integrand == "peak":
+        keep = mcb.Program("exp(-100*((x1-c)^2+(x2-c)^2))", 2, ["c"])
+        cs = [0.3 + 0.4 * i / max(1, args.fns - 1) for i in range(args.fns)]
+        fns = [mcb.tree(keep.integrand({"c": c}, n_samples=args.budget, index=i), samples_per_cell=args.spc)
+               for i, c in enumerate(cs)]
+        sources = [f"exp(-100*((x1-{c!r})^2+(x2-{c!r})^2))" for c in cs]
+    else:
+        fns = [mcb.tree(mcb.harmonic(w.harmonic_k(n), 4, unit_coeffs=True, n_samples=args.budget, index=i),
+                        samples_per_cell=args.spc)
+               for i, n in enumerate(list(range(1, 101)) * ((args.fns + 99) // 100))][:args.fns]
     for i, f in enumerate(fns):
         f.integrand_index = i
     seed = 20200814
@@ -45,7 +55,7 @@ def main():
         times.append(time.perf_counter() - t0)
     t = min(times)
     drawn = int(out["n_samples"].sum())
-    res = {"workload": f"{args.fns} Fig.1 harmonic trees x {args.trials} trials, budget {args.budget}, "
+    res = {"workload": f"{args.fns} {args.integrand} trees x {args.trials} trials, budget {args.budget}, "
                        f"spc {args.spc}",
            "seconds": t, "samples_drawn": drawn, "samples_per_s": drawn / t,
            "leaves_mean": float(out["n_cells"].mean()), "max_depth": int(out["max_depth"].max()),
@@ -54,7 +64,8 @@ def main():
     from tests import _oracle
     if args.ref_fns and _oracle.load_ref() is not None:
         sub = fns[:args.ref_fns]
-        o, _, _, _, secs = _oracle.ref_run_batch(sub, seed, args.trials, workers=0)
+        o, _, _, _, secs = _oracle.ref_run_batch(sub, seed, args.trials, workers=0,
+                                                 sources=sources[:args.ref_fns] if sources else None)
         rdrawn = int(o["n_samples"].sum())
         res["reference_cpu"] = {"fns": len(sub), "threads": os.cpu_count(), "seconds": secs,
                                 "samples_per_s": rdrawn / secs}
