@@ -335,6 +335,20 @@ int ref_results_roundtrip(const char* in_path, const char* out_path) {
   }
 }
 
+// run_command (src/job_io.cpp): the reference CLI's `run` (tools/mcbatch.cpp
+// needs CLI11, absent from the image; its `run` is this call).  workers < 0
+// keeps the job's own worker count.
+int ref_run_command(const char* job_path, const char* out_path, int workers) {
+  try {
+    RunOverrides ov;
+    if (workers >= 0) ov.workers = std::uint32_t(workers);
+    return run_command(job_path, out_path, ov);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 double ref_harmonic_closed_form(double k) { return harmonic_closed_form(k); }
 double ref_analytic_harmonic(std::uint32_t n) { return analytic_harmonic(n); }
 

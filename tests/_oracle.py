@@ -192,6 +192,7 @@ def load_ref():
         "ref_analytic_harmonic": (dbl, [u32]),
         "ref_job_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
         "ref_results_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
+        "ref_run_command": (i32, [ctypes.c_char_p, ctypes.c_char_p, i32]),
         "ref_tree_refine_source": (i32, [ctypes.c_char_p, P(Integrand), P(ctypes.c_char_p), P(dbl), sz, u64,
                                          u32, u64, P(TrialStats), P(Leaf), sz, P(sz)]),
     }
