@@ -71,6 +71,9 @@ uint64_t splitmix64(uint64_t z) {  // src/sampling.cpp:44-49
 
 uint64_t chunk_count(uint64_t n) { return (n + MCB_CHUNK_SIZE - 1) / MCB_CHUNK_SIZE; }
 
+template <class T>
+T round_up(T v, T m) { return (v + m - 1) / m * m; }
+
 // ---- stratified plan (ref src/batch.cpp:41-54, src/estimator.cpp:94-122) ----
 
 // cell_grid_size: k^d, failing past the cap (CellBudgetExceeded).
@@ -338,6 +341,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
     d.spc = sp.spc;
     d.cpc = uint32_t(chunk_count(sp.spc));
     d.n_chunks = d.n_cells * d.cpc;
+    if (sp.spc <= kWarpTileMaxSpc) d.n_chunks = round_up(d.n_chunks, kTileAlign);  // warp per tile
     cell_k = double(sp.k);
   }
   d.chunk_base = chunk_base;
@@ -369,6 +373,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
     // interpreter: plain parameters, unscaled draws, non-finite counting
     for (uint32_t j = 0; j < MCB_MAX_DIM; ++j) d.k[j] = f.k[j];
     p.variant = kSafe | (unit_dom ? kUnitDomain : 0) | (strat ? kStrat : 0);
+    if (stratified(f) && d.spc <= kWarpTileMaxSpc) p.variant |= kWarpTile;
     double mid[MCB_MAX_DIM];
     for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
     const double c = host_eval(f, mid);
@@ -425,6 +430,7 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   if (!harm) p.variant &= ~kUnitCoef;
   if (strat) p.variant |= kStrat;
   if (tree_cells) p.variant &= ~kNoShift;  // cells shrink: keep the per-tile shift
+  if (stratified(f) && d.spc <= kWarpTileMaxSpc) p.variant |= kWarpTile;
   // shift constant: f at the domain midpoint (reference op order, libm)
   double mid[MCB_MAX_DIM];
   for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
@@ -541,10 +547,11 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
   for (size_t r = 0; r < n_fns; ++r) {
     const size_t i = order[r];
     FnDesc d = prep[i].d;
+    const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
+    if (var & mcb::detail::kWarpTile) tile = round_up<uint64_t>(tile, mcb::detail::kTileAlign);
     d.tile_base = tile;
     d.out_slot = i;
     const uint64_t nt = uint64_t(d.n_chunks) * trials;
-    const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
     uint32_t slots = 0;
     if (fam == MCB_FAMILY_PROGRAM) {
       const mcb_program* pg = fns[i].program;
@@ -753,6 +760,7 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
   for (size_t i = 0; i < n; ++i) {
     const mcb::tree::CellBatch& b = *batches[i];
     prep[i] = prepare(*b.fn, seed, uint32_t(b.chunk_base), b.trial, true);
+    if (b.spc <= mcb::detail::kWarpTileMaxSpc) prep[i].variant |= mcb::detail::kWarpTile;
     n_rects += size_t(b.n_cells) * 2 * b.fn->dim;
     n_cells += b.n_cells;
   }
@@ -762,8 +770,9 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
     return std::make_tuple(batches[x]->fn->family, batches[x]->fn->dim, prep[x].variant) <
            std::make_tuple(batches[y]->fn->family, batches[y]->fn->dim, prep[y].variant);
   });
-  uint64_t tiles = 0;
-  for (size_t i = 0; i < n; ++i) tiles += uint64_t(batches[i]->n_cells) * chunk_count(batches[i]->spc);
+  uint64_t tiles = 0;  // upper bound incl. warp-tile padding and alignment
+  for (size_t i = 0; i < n; ++i)
+    tiles += uint64_t(batches[i]->n_cells) * chunk_count(batches[i]->spc) + 2 * mcb::detail::kTileAlign;
 
   DeviceCtx& c = device_ctx(device);
   std::lock_guard<std::mutex> lock(c.mu);
@@ -805,6 +814,10 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
     d.cpc = uint32_t(chunk_count(b.spc));
     d.n_chunks = d.n_cells * d.cpc;
     d.n_samples = uint64_t(b.n_cells) * b.spc;
+    if (prep[i].variant & mcb::detail::kWarpTile) {
+      d.n_chunks = round_up<uint32_t>(d.n_chunks, mcb::detail::kTileAlign);
+      tile = round_up<uint64_t>(tile, mcb::detail::kTileAlign);
+    }
     d.tile_base = tile;
     d.out_slot = r;
     d.cell_rects = c.buf.rects + rect_at;
@@ -1167,7 +1180,13 @@ mcb_status mcb_plan_get_info(const mcb_plan* plan, mcb_plan_info* info) {
   info->total_samples = plan->hp.total_samples;
   info->philox_blocks = plan->hp.philox_blocks;
   uint32_t launches = 1;  // k_combine
-  for (const auto& g : plan->hp.groups) launches += uint32_t((g.n_tiles + 0x7FFFFFFEull) / 0x7FFFFFFFull);
+  for (const auto& g : plan->hp.groups) {
+    const uint64_t ctas = g.n_tiles / ((g.variant & mcb::detail::kWarpTile)
+                                           ? (g.family == MCB_FAMILY_PROGRAM ? uint64_t(mcb::detail::kProgThreads / 32)
+                                                                             : uint64_t(mcb::detail::kTileAlign))
+                                           : 1u);
+    launches += uint32_t((ctas + 0x7FFFFFF7ull) / 0x7FFFFFF8ull);
+  }
   info->launches_per_run = launches;
   return MCB_OK;
 }

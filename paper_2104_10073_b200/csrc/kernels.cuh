@@ -170,6 +170,93 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
   }
 }
 
+// K3w k_direct_warp<FAM,D,V> (V has kStrat | kWarpTile): small cells.  The
+// CTA covers kTileAlign consecutive tiles of ONE (integrand, trial) (the host
+// pads each integrand's per-trial tile range to a multiple of kTileAlign), so
+// the descriptor and the trig table stay CTA-uniform while each warp runs one
+// tile start to finish: per-warp shift (lane 0, broadcast), lane-strided
+// pairs, warp butterfly, one TilePartial per tile — no CTA barrier after the
+// table.  Same sums per tile as K3 up to the (fixed) reduction shape.
+template <int FAM, int D, int V>
+__global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
+    k_direct_warp(const FnDesc* __restrict__ fns, const uint32_t* __restrict__ tile_fn, uint64_t tile0,
+                  TilePartial* __restrict__ part) {
+  constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
+  constexpr bool SAFE = (V & kSafe) != 0;
+  constexpr bool NOSHIFT = (V & kNoShift) != 0;
+  constexpr bool HARM = FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC;
+  constexpr bool TABLE = HARM && !SAFE;
+  static_assert((V & kStrat) && (V & kWarpTile), "cell-structured warp-tile variant");
+
+  const uint64_t group = tile0 + uint64_t(blockIdx.x) * kTileAlign;
+  const uint32_t fi = __ldg(tile_fn + group);
+  FnDesc f = fns[fi];
+  __shared__ TrigAB ab[TABLE ? 512 : 1];
+  if (TABLE) {
+    build_trig_table<UNIT_COEF>(ab, f.a, f.b);
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t tile = group + warp;
+  const uint32_t rem = uint32_t(tile - f.tile_base);
+  const uint32_t trial = rem / f.n_chunks;
+  const uint32_t chunk = rem - trial * f.n_chunks;
+  const uint32_t cell = chunk / f.cpc, cc = chunk - cell * f.cpc;
+  if (cell >= f.n_cells) return;  // padding tile of the aligned range
+  const uint32_t count = (cc + 1 == f.cpc) ? f.spc - cc * MCB_CHUNK_SIZE : MCB_CHUNK_SIZE;
+  dev::cell_rect<D>(f, cell, SAFE ? 1.0 : dev::kTwoM64);
+  const uint32_t pairs = (count + 1) >> 1;
+  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
+  if (!NOSHIFT) {  // per-tile shift = f(first sample of the tile), as K3
+    double f0 = 0.0;
+    if (lane == 0) {
+      double st0, st1;
+      dev::gen_pair<FAM, D, false, SAFE>(f, P, 0ull, st0, st1);
+      f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, st0);
+      f0 = finite64(f0) ? f0 : 0.0;
+    }
+    f.shift = __shfl_sync(0xFFFFFFFFu, f0, 0);
+  }
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t nbad = 0;
+  for (uint32_t q = lane; q < pairs; q += 32) {
+    double x0, x1;
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(q * uint32_t(D)), x0, x1);
+    const double f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
+    const double f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
+    const bool has1 = 2 * q + 1 < count;
+    double g0 = NOSHIFT ? f0 : __dsub_rn(f0, f.shift);
+    double g1 = NOSHIFT ? f1 : __dsub_rn(f1, f.shift);
+    if (SAFE) {
+      const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
+      nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+      g0 = ok0 ? g0 : 0.0;
+      g1 = ok1 ? g1 : 0.0;
+    } else {
+      g1 = has1 ? g1 : 0.0;
+    }
+    s1 = __dadd_rn(s1, g0);
+    s2 = fma(g0, g0, s2);
+    s1 = __dadd_rn(s1, g1);
+    s2 = fma(g1, g1, s2);
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    s1 = __dadd_rn(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, m));
+    s2 = __dadd_rn(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, m));
+    if (SAFE) nbad += __shfl_xor_sync(0xFFFFFFFFu, nbad, m);
+  }
+  if (lane == 0) {
+    TilePartial p;
+    p.s1 = s1;
+    p.s2 = s2;
+    p.shift = NOSHIFT ? 0.0 : f.shift;
+    p.n_nonfinite = SAFE ? nbad : 0u;
+    p.n_finite = count - p.n_nonfinite;
+    part[tile] = p;
+  }
+}
+
 // Family values of the pairs [first_pair, first_pair + n_pairs) of one chunk,
 // through exactly the gen_pair/finish instantiation the fused kernel uses.
 template <int FAM, int D, int V>
@@ -206,7 +293,7 @@ struct Entry {
 };
 
 struct Table {
-  Entry e[4][MCB_MAX_DIM + 1][32];
+  Entry e[4][MCB_MAX_DIM + 1][64];
   template <int FAM, int D, int V>
   void put() {
     e[FAM][D][V].direct = k_direct<FAM, D, V>;
@@ -217,6 +304,7 @@ struct Table {
   template <int FAM, int D, int V>
   void put_run() {
     e[FAM][D][V | kStrat].direct = k_direct<FAM, D, V | kStrat>;
+    e[FAM][D][V | kStrat | kWarpTile].direct = k_direct_warp<FAM, D, V | kStrat | kWarpTile>;
   }
 };
 

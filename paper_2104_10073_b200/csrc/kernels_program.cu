@@ -239,6 +239,77 @@ __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
   }
 }
 
+// Small cells (kStrat | kWarpTile): the CTA covers kProgThreads/32 tiles of
+// one (integrand, trial) — the host pads per-trial tile ranges to multiples
+// of kTileAlign — so the staged program stays CTA-uniform while each warp
+// runs one tile: per-warp shift, lane-strided pairs, warp butterfly.
+template <int D, int V>
+__global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ fns,
+                                                    const uint32_t* __restrict__ tile_fn, uint64_t tile0,
+                                                    TilePartial* __restrict__ part,
+                                                    const uint32_t* __restrict__ code,
+                                                    const double* __restrict__ consts, uint32_t slots) {
+  static_assert((V & kStrat) && (V & kWarpTile), "cell-structured warp-tile variant");
+  constexpr uint32_t kTilesPerCta = T / 32;
+  const uint64_t group = tile0 + uint64_t(blockIdx.x) * kTilesPerCta;
+  const uint32_t fi = __ldg(tile_fn + group);
+  FnDesc f = fns[fi];
+  __shared__ double params[prog::kMaxParams];
+  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t tile = group + warp;
+  const uint32_t rem = uint32_t(tile - f.tile_base);
+  const uint32_t trial = rem / f.n_chunks;
+  const uint32_t chunk = rem - trial * f.n_chunks;
+  const uint32_t cell = chunk / f.cpc, cc = chunk - cell * f.cpc;
+  if (cell >= f.n_cells) return;  // padding tile of the aligned range
+  const uint32_t count = (cc + 1 == f.cpc) ? f.spc - cc * MCB_CHUNK_SIZE : MCB_CHUNK_SIZE;
+  dev::cell_rect<D>(f, cell, 1.0);
+  const uint32_t pairs = (count + 1) >> 1;
+  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
+  {  // per-tile shift = f(first sample of the tile)
+    double f0 = 0.0;
+    if (lane == 0) {
+      gen_points<D, false>(f, P, 0, m.X);
+      interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+      f0 = m.S[threadIdx.x];
+      f0 = finite64(f0) ? f0 : 0.0;
+    }
+    f.shift = __shfl_sync(0xFFFFFFFFu, f0, 0);
+  }
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t nbad = 0;
+  for (uint32_t q = lane; q < pairs; q += 32) {
+    gen_points<D, false>(f, P, q, m.X);
+    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+    const double f0 = m.S[threadIdx.x], f1 = m.S[T + threadIdx.x];
+    const bool has1 = 2 * q + 1 < count;
+    const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
+    nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+    const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
+    const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
+    s1 = __dadd_rn(s1, g0);
+    s2 = fma(g0, g0, s2);
+    s1 = __dadd_rn(s1, g1);
+    s2 = fma(g1, g1, s2);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    s1 = __dadd_rn(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, o));
+    s2 = __dadd_rn(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, o));
+    nbad += __shfl_xor_sync(0xFFFFFFFFu, nbad, o);
+  }
+  if (lane == 0) {
+    TilePartial p;
+    p.s1 = s1;
+    p.s2 = s2;
+    p.shift = f.shift;
+    p.n_nonfinite = nbad;
+    p.n_finite = count - nbad;
+    part[tile] = p;
+  }
+}
+
 // Per-sample values of pairs [first_pair, first_pair + n_pairs) of one chunk
 // (test hook): exactly the gen_points/interp_pair of k_program.
 template <int D, int V>
@@ -274,12 +345,13 @@ struct ProgEntry {
 };
 
 struct ProgTable {
-  ProgEntry e[MCB_MAX_DIM + 1][3];  // general domain, unit domain, stratified
+  ProgEntry e[MCB_MAX_DIM + 1][4];  // general domain, unit domain, cells, small cells
   template <int D>
   void put() {
     e[D][0] = {k_program<D, kSafe>, k_program_eval<D, kSafe>};
     e[D][1] = {k_program<D, kSafe | kUnitDomain>, k_program_eval<D, kSafe | kUnitDomain>};
     e[D][2] = {k_program<D, kSafe | kStrat>, k_program_eval<D, kSafe>};
+    e[D][3] = {k_program_warp<D, kSafe | kStrat | kWarpTile>, k_program_eval<D, kSafe>};
   }
   ProgTable() {
     put<1>();
@@ -310,7 +382,7 @@ static cudaError_t ensure_smem_optin() {
   if (done.count(dev)) return cudaSuccess;
   const ProgTable& t = prog_table();
   for (int d = 1; d <= int(MCB_MAX_DIM); ++d)
-    for (int v = 0; v < 3; ++v) {
+    for (int v = 0; v < 4; ++v) {
       const int smem = int(program_smem_bytes(prog::kMaxDepth, d));
       if ((e = cudaFuncSetAttribute(t.e[d][v].run, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem)) != cudaSuccess)
@@ -325,7 +397,7 @@ static cudaError_t ensure_smem_optin() {
 
 static const ProgEntry* prog_entry(int dim, int variant) {
   if (dim < 1 || dim > int(MCB_MAX_DIM)) return nullptr;
-  return &prog_table().e[dim][(variant & kStrat) ? 2 : (variant & kUnitDomain) ? 1 : 0];
+  return &prog_table().e[dim][(variant & kWarpTile) ? 3 : (variant & kStrat) ? 2 : (variant & kUnitDomain) ? 1 : 0];
 }
 
 cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const uint32_t* tile_fn,
@@ -335,11 +407,13 @@ cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const 
   if (!e) return cudaErrorInvalidValue;
   if (cudaError_t err = ensure_smem_optin(); err != cudaSuccess) return err;
   const size_t smem = program_smem_bytes(g.slots, g.dim);
-  const uint64_t kMaxGrid = 0x7FFFFFFFull;
-  for (uint64_t off = 0; off < g.n_tiles; off += kMaxGrid) {
-    const uint64_t n = g.n_tiles - off < kMaxGrid ? g.n_tiles - off : kMaxGrid;
-    e->run<<<dim3(uint32_t(n)), dim3(T), smem, s>>>(fns, tile_fn, g.tile0 + off, part, code, consts,
-                                                      g.slots);
+  const uint64_t per_cta = (g.variant & kWarpTile) ? uint64_t(T / 32) : 1u;  // tiles per CTA
+  const uint64_t n_ctas = g.n_tiles / per_cta;
+  const uint64_t kMaxGrid = 0x7FFFFFF8ull;
+  for (uint64_t off = 0; off < n_ctas; off += kMaxGrid) {
+    const uint64_t n = n_ctas - off < kMaxGrid ? n_ctas - off : kMaxGrid;
+    e->run<<<dim3(uint32_t(n)), dim3(T), smem, s>>>(fns, tile_fn, g.tile0 + off * per_cta, part, code,
+                                                      consts, g.slots);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }

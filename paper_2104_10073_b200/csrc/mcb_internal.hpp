@@ -33,9 +33,21 @@ enum Variant : int {
                     // the FAST preconditions, see capi.cpp prepare())
   kNoShift = 8,     // harmonic FAST: accumulate f itself (the host proved the
                     // integrand far from constant, so no cancellation)
-  kStrat = 16       // STRATIFIED method: tiles are (trial, cell, chunk), the
+  kStrat = 16,      // STRATIFIED method: tiles are (trial, cell, chunk), the
                     // cell rectangle is derived on the device (grid_cell)
+  kWarpTile = 32    // with kStrat, small cells: one WARP per tile, so a CTA
+                    // covers kTileAlign tiles of one (integrand, trial); each
+                    // integrand's per-trial tile range is padded to a
+                    // multiple of kTileAlign and its tile_base aligned
 };
+
+// Tile alignment of kWarpTile integrands (= warps of the family kernel's CTA,
+// a multiple of the interpreter's 4 warps) and the cell size up to which
+// cell-structured integrands use it.
+constexpr uint32_t kTileAlign = 8;
+constexpr uint32_t kWarpTileMaxSpc = 8192;
+static_assert(kThreads / 32 == int(kTileAlign), "family CTA = kTileAlign warps");
+static_assert(kTileAlign % (kProgThreads / 32) == 0, "interpreter CTAs tile the aligned groups");
 
 // One kernel launch = one (family, dim, variant) group of integrands whose
 // tiles are contiguous in the plan's tile space.
