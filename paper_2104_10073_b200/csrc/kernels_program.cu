@@ -145,7 +145,11 @@ __device__ __forceinline__ ProgramSmem stage_program(const FnDesc& f, const uint
   m.code = reinterpret_cast<uint32_t*>(m.consts + prog::kMaxConsts);
   for (uint32_t i = threadIdx.x; i < 2 * f.prog_len; i += T) m.code[i] = code[f.prog_off + i];
   for (uint32_t i = threadIdx.x; i < f.n_consts; i += T) m.consts[i] = consts[f.const_off + i];
-  if (threadIdx.x < prog::kMaxParams) params[threadIdx.x] = f.k[threadIdx.x];
+  // static indices only: a dynamic f.k[threadIdx.x] would demote the whole
+  // descriptor copy to local memory
+#pragma unroll
+  for (int i = 0; i < int(prog::kMaxParams); ++i)
+    if (threadIdx.x == i) params[i] = f.k[i];
   __syncthreads();
   return m;
 }

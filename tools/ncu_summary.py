@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Summarise an ncu --set full report of k_direct: pipe utilisation, issue,
+"""Summarise an ncu --set full report (every profiled launch): pipe utilisation, issue,
 stalls, DRAM traffic.  Usage: tools/ncu_summary.py report.ncu-rep > summary.txt"""
 import csv
 import io
@@ -35,12 +35,15 @@ def main():
     raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, vals = rows[0], rows[2]
-    d = dict(zip(hdr, vals))
-    print(f"kernel: {d.get('Kernel Name', '?')}")
-    for k, label in KEYS:
-        if k in d:
-            print(f"  {label:28s} {d[k]}")
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:  # one row per profiled launch
+        d = dict(zip(hdr, vals))
+        u = dict(zip(hdr, units))
+        print(f"kernel: {d.get('Kernel Name', '?')}")
+        for k, label in KEYS:
+            if k in d:
+                unit = f" {u[k]}" if u.get(k) else ""
+                print(f"  {label:28s} {d[k]}{unit}")
 
 
 if __name__ == "__main__":
