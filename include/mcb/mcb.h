@@ -277,6 +277,16 @@ MCB_API mcb_status mcb_debug_points(uint64_t seed, uint32_t integrand_index, uin
 MCB_API mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
                           uint64_t chunk, uint64_t first_point, uint64_t count,
                           int device, double* out);
+/* Runtime specialisation of PROGRAM integrands: each program is compiled by
+ * NVRTC into straight-line sm_100a code (bit-identical results to the
+ * bytecode interpreter, which runs when this is off or NVRTC is missing).
+ * mode 1 = on (default unless MCB_PROGRAM_JIT=0), 0 = off, < 0 = query;
+ * returns whether it is active.  Compiled cubins are cached in memory per
+ * device and on disk ($MCB_JIT_CACHE, default ~/.cache/mcb-jit; "0" = off). */
+MCB_API int mcb_program_jit(int mode);
+/* NVRTC compilations so far, and the last JIT failure ("" if none). */
+MCB_API uint64_t mcb_program_jit_compiles(void);
+MCB_API size_t mcb_program_jit_error(char* buf, size_t cap);
 /* Roofline probe: Philox4x32-10 blocks per second that `device` can generate
  * with no integrand work at all (same generator code as the fused kernel),
  * timed over ~`ms` milliseconds.  The denominator of bench.py's roofline. */

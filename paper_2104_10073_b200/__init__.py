@@ -107,7 +107,8 @@ ABI_SYMBOLS = [
     "mcb_direct_mc", "mcb_plan_create", "mcb_plan_launch", "mcb_plan_download",
     "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
     "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
-    "mcb_program_param_name", "mcb_stratified_plan", "mcb_tree_refine",
+    "mcb_program_param_name", "mcb_stratified_plan", "mcb_tree_refine", "mcb_program_jit",
+    "mcb_program_jit_compiles", "mcb_program_jit_error",
 ]
 
 
@@ -146,6 +147,9 @@ def _load() -> ctypes.CDLL:
         "mcb_program_param_name": (sz, [vp, u32, ctypes.c_char_p, sz]),
         "mcb_stratified_plan": (i32, [P(Integrand), P(u32), P(u64), P(u32)]),
         "mcb_tree_refine": (i32, [P(Integrand), u64, u32, u64, i32, P(TrialStats), P(Leaf), sz, P(sz)]),
+        "mcb_program_jit": (i32, [i32]),
+        "mcb_program_jit_compiles": (u64, []),
+        "mcb_program_jit_error": (sz, [ctypes.c_char_p, sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -415,6 +419,22 @@ def debug_eval(f: Integrand, seed: int, trial: int, chunk: int, first_point: int
     _check(lib.mcb_debug_eval(ctypes.byref(f), seed, trial, chunk, first_point, count, device,
                               out.ctypes.data))
     return out
+
+
+def program_jit(mode: int = -1) -> bool:
+    """Runtime specialisation of DSL programs (NVRTC): 1 on, 0 off (bytecode
+    interpreter), -1 query.  Returns whether it is active."""
+    return bool(lib.mcb_program_jit(mode))
+
+
+def program_jit_compiles() -> int:
+    return int(lib.mcb_program_jit_compiles())
+
+
+def program_jit_error() -> str:
+    buf = ctypes.create_string_buffer(lib.mcb_program_jit_error(None, 0))
+    lib.mcb_program_jit_error(buf, len(buf))
+    return buf.value.decode()
 
 
 def probe_philox_peak(device: int = 0, ms: float = 50.0) -> float:

@@ -30,6 +30,7 @@
 
 #include "mcb/mcb.h"
 #include "mcb_internal.hpp"
+#include "jit.hpp"
 #include "program.hpp"
 #include "tree.hpp"
 
@@ -536,9 +537,14 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
                       trial_bases ? trial_bases[i] : trial_base);
   std::vector<size_t> order(n_fns);
   std::iota(order.begin(), order.end(), size_t(0));
+  // groups: (family, dim, variant), and one group per program for PROGRAM
+  // integrands (each program launches its own specialised kernel)
+  auto prog_key = [&](size_t i) {
+    return fns[i].family == MCB_FAMILY_PROGRAM ? reinterpret_cast<uintptr_t>(fns[i].program) : uintptr_t(0);
+  };
   std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
-    auto kx = std::make_tuple(fns[x].family, fns[x].dim, prep[x].variant);
-    auto ky = std::make_tuple(fns[y].family, fns[y].dim, prep[y].variant);
+    auto kx = std::make_tuple(fns[x].family, fns[x].dim, prep[x].variant, prog_key(x));
+    auto ky = std::make_tuple(fns[y].family, fns[y].dim, prep[y].variant, prog_key(y));
     return kx < ky;
   });
   hp.descs.resize(n_fns);
@@ -567,9 +573,10 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
       d.n_consts = uint32_t(pg->p.consts.size());
       slots = pg->p.depth;
     }
+    const mcb::prog::Program* gp = fam == MCB_FAMILY_PROGRAM ? &fns[i].program->p : nullptr;
     if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
-        hp.groups.back().variant != var)
-      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0});
+        hp.groups.back().variant != var || hp.groups.back().prog != gp)
+      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0, gp});
     hp.groups.back().n_tiles += nt;
     hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
     tile += nt;
@@ -641,9 +648,19 @@ struct DevBuf {
 
 // Enqueue: descriptor upload (from `staged`, pinned or not) + tile table +
 // fused kernels + ordered combine, all on `s`.
+// Runtime-specialised kernels of the plan's programs, compiled in parallel
+// before the first launch (jit.hpp).
+void prepare_programs(const HostPlan& hp) {
+  std::vector<const mcb::prog::Program*> progs;
+  for (const auto& g : hp.groups)
+    if (g.prog && std::find(progs.begin(), progs.end(), g.prog) == progs.end()) progs.push_back(g.prog);
+  mcb::jit::prepare(progs);
+}
+
 mcb_status enqueue_run(const HostPlan& hp, DevBuf& buf, uint32_t trials, const FnDesc* staged,
                        bool upload, cudaStream_t s) {
   cudaError_t e;
+  if (upload) prepare_programs(hp);
   const uint32_t n_fns = uint32_t(hp.descs.size());
   if (upload) {
     if ((e = cudaMemcpyAsync(buf.fns, staged, sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -766,9 +783,13 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
   }
   std::vector<size_t> order(n);
   std::iota(order.begin(), order.end(), size_t(0));
+  auto prog_key = [&](size_t i) {
+    return batches[i]->fn->family == MCB_FAMILY_PROGRAM ? reinterpret_cast<uintptr_t>(batches[i]->fn->program)
+                                                        : uintptr_t(0);
+  };
   std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
-    return std::make_tuple(batches[x]->fn->family, batches[x]->fn->dim, prep[x].variant) <
-           std::make_tuple(batches[y]->fn->family, batches[y]->fn->dim, prep[y].variant);
+    return std::make_tuple(batches[x]->fn->family, batches[x]->fn->dim, prep[x].variant, prog_key(x)) <
+           std::make_tuple(batches[y]->fn->family, batches[y]->fn->dim, prep[y].variant, prog_key(y));
   });
   uint64_t tiles = 0;  // upper bound incl. warp-tile padding and alignment
   for (size_t i = 0; i < n; ++i)
@@ -837,9 +858,10 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
       d.n_consts = uint32_t(b.fn->program->p.consts.size());
       slots = b.fn->program->p.depth;
     }
+    const mcb::prog::Program* gp = fam == MCB_FAMILY_PROGRAM ? &b.fn->program->p : nullptr;
     if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
-        hp.groups.back().variant != var)
-      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0});
+        hp.groups.back().variant != var || hp.groups.back().prog != gp)
+      hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0, gp});
     hp.groups.back().n_tiles += d.n_chunks;
     hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
     tile += d.n_chunks;
@@ -911,6 +933,7 @@ mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t see
   if (e == cudaSuccess && !plan->hp.consts.empty())
     e = cudaMemcpy(plan->buf.consts, plan->hp.consts.data(), sizeof(double) * plan->hp.consts.size(),
                    cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) prepare_programs(plan->hp);
   if (e == cudaSuccess)
     e = mcb::detail::launch_expand_tiles(plan->buf.fns, uint32_t(n_fns), trials, plan->buf.tile_fn, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -1380,6 +1403,23 @@ mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial
   if (e != cudaSuccess) return cuda_fail(e, "debug_eval");
   std::memcpy(out, tmp.data() + (first_point - 2 * first_pair), sizeof(double) * count);
   return MCB_OK;
+}
+
+int mcb_program_jit(int mode) {
+  if (mode >= 0) mcb::jit::set_enabled(mode != 0);
+  return mcb::jit::enabled() ? 1 : 0;
+}
+
+uint64_t mcb_program_jit_compiles(void) { return mcb::jit::compile_count(); }
+
+size_t mcb_program_jit_error(char* buf, size_t cap) {
+  const std::string s = mcb::jit::last_error();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return s.size() + 1;
 }
 
 mcb_status mcb_probe_philox_peak(int device, double ms, double* blocks_per_s) {

@@ -1,0 +1,54 @@
+// jit.hpp — runtime specialisation of DSL programs (MCB_FAMILY_PROGRAM).
+//
+// A compiled program (program.hpp) is emitted as straight-line CUDA
+// (prog::emit_cuda), compiled by NVRTC for sm_100a together with the
+// jit_kernels.cuh templates (their text and the headers they need are
+// embedded in libmcb.so at build time), loaded into the current device's
+// primary context and launched instead of the bytecode interpreter.  Results
+// are bit-identical to the interpreter's (same operations, same sample order
+// and reduction shape).  Modules are cached per (device, program source).
+// When NVRTC cannot be loaded or a compile fails, the interpreter kernels
+// run instead — both are the sm_100a GPU path; there is no CPU path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace mcb {
+namespace prog {
+struct Program;
+}
+namespace dev {
+struct FnDesc;
+struct TilePartial;
+}
+namespace jit {
+
+// Process-wide switch: MCB_PROGRAM_JIT=0 in the environment disables it;
+// set_enabled() overrides.  enabled() is false when NVRTC is unavailable.
+bool enabled();
+void set_enabled(bool on);
+// Why the last compile or the NVRTC load failed ("" if none).
+std::string last_error();
+
+// Launch the specialised kernel of `p` in `mode` (0 direct, 1 direct on the
+// unit cube, 2 cells CTA-per-tile, 3 small cells warp-per-tile) over `ctas`
+// CTAs of 128 threads starting at tile `tile0`.  Returns false (nothing
+// launched) when JIT is off or the program could not be compiled, so the
+// caller runs the interpreter.
+bool launch(const prog::Program& p, int mode, uint32_t ctas, const dev::FnDesc* fns, const uint32_t* tile_fn,
+            uint64_t tile0, dev::TilePartial* part, cudaStream_t s, cudaError_t* err);
+
+// Compile (in parallel) and load the specialised modules of `programs` that
+// the current device does not have yet; launch() would otherwise compile
+// them one by one on first use.
+void prepare(const std::vector<const prog::Program*>& programs);
+
+// Number of NVRTC compilations performed so far (tests / tracing).
+uint64_t compile_count();
+
+}  // namespace jit
+}  // namespace mcb

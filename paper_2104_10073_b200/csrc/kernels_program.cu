@@ -23,6 +23,7 @@
 #include <mutex>
 #include <set>
 
+#include "jit.hpp"
 #include "kernels.cuh"
 #include "program.hpp"
 
@@ -409,11 +410,16 @@ cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const 
                                  cudaStream_t s) {
   const ProgEntry* e = prog_entry(g.dim, g.variant);
   if (!e) return cudaErrorInvalidValue;
-  if (cudaError_t err = ensure_smem_optin(); err != cudaSuccess) return err;
-  const size_t smem = program_smem_bytes(g.slots, g.dim);
   const uint64_t per_cta = (g.variant & kWarpTile) ? uint64_t(T / 32) : 1u;  // tiles per CTA
   const uint64_t n_ctas = g.n_tiles / per_cta;
   const uint64_t kMaxGrid = 0x7FFFFFF8ull;
+  if (g.prog && n_ctas <= kMaxGrid) {  // runtime-specialised kernel of this program (jit.hpp)
+    const int mode = (g.variant & kWarpTile) ? 3 : (g.variant & kStrat) ? 2 : (g.variant & kUnitDomain) ? 1 : 0;
+    cudaError_t err = cudaSuccess;
+    if (jit::launch(*g.prog, mode, uint32_t(n_ctas), fns, tile_fn, g.tile0, part, s, &err)) return err;
+  }
+  if (cudaError_t err = ensure_smem_optin(); err != cudaSuccess) return err;
+  const size_t smem = program_smem_bytes(g.slots, g.dim);
   for (uint64_t off = 0; off < n_ctas; off += kMaxGrid) {
     const uint64_t n = n_ctas - off < kMaxGrid ? n_ctas - off : kMaxGrid;
     e->run<<<dim3(uint32_t(n)), dim3(T), smem, s>>>(fns, tile_fn, g.tile0 + off * per_cta, part, code,

@@ -11,6 +11,9 @@
 #include "mcb_device.cuh"
 
 namespace mcb {
+namespace prog {
+struct Program;
+}
 namespace detail {
 
 #ifndef MCB_THREADS
@@ -55,6 +58,7 @@ struct GroupLaunch {
   int family, dim, variant;
   uint64_t tile0, n_tiles;
   uint32_t slots = 0;  // PROGRAM family: max stack depth of the group's programs
+  const prog::Program* prog = nullptr;  // PROGRAM family: the group's one program (runtime-specialised)
 };
 
 bool variant_supported(int family, int dim, int variant);

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cctype>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -534,6 +535,59 @@ double evaluate(const Program& p, const double* x, const double* params) {
     st[i.dst] = r;
   }
   return st[0];
+}
+
+std::string emit_cuda(const Program& p, const std::string& name) {
+  auto opnd = [&](const Operand& o) -> std::string {
+    char buf[64];
+    switch (o.kind) {
+      case kVar: std::snprintf(buf, sizeof buf, "x[%u]", o.index); break;
+      case kParam: std::snprintf(buf, sizeof buf, "p[%u]", o.index); break;
+      case kConst: {
+        uint64_t bits;
+        std::memcpy(&bits, &p.consts[o.index], 8);
+        std::snprintf(buf, sizeof buf, "__longlong_as_double((long long)0x%016llxull)",
+                      (unsigned long long)bits);
+        break;
+      }
+      default: std::snprintf(buf, sizeof buf, "s%u", o.index); break;
+    }
+    return buf;
+  };
+  static const char* const unary[] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                      "sin", "cos", "tan", "asin", "acos", "atan", "exp", "log",
+                                      "__dsqrt_rn", "fabs", "floor"};
+  std::string o = "struct " + name + " {\n  static __device__ __forceinline__ double eval(const double* x, "
+                  "const double* p) {\n";
+  const uint32_t slots = std::max<uint32_t>(p.depth, 1);
+  o += "    double";
+  for (uint32_t i = 0; i < slots; ++i) o += (i ? ", s" : " s") + std::to_string(i) + " = 0.0";
+  o += ";\n    (void)x; (void)p;\n";
+  for (const Instr& i : p.code) {
+    const std::string d = "s" + std::to_string(i.dst), a = opnd(i.a), b = opnd(i.b);
+    switch (i.op) {
+      case kCopy: o += "    " + d + " = " + a + ";\n"; break;
+      case kSinCos:  // second result first, as the interpreter stores it
+        o += "    { double sn_, cs_; sincos(" + a + ", &sn_, &cs_); s" + std::to_string(i.dst2) + " = cs_; " + d +
+             " = sn_; }\n";
+        break;
+      case kNeg: o += "    " + d + " = -(" + a + ");\n"; break;
+      case kAdd: o += "    " + d + " = __dadd_rn(" + a + ", " + b + ");\n"; break;
+      case kSub: o += "    " + d + " = __dsub_rn(" + a + ", " + b + ");\n"; break;
+      case kMul: o += "    " + d + " = __dmul_rn(" + a + ", " + b + ");\n"; break;
+      case kDiv: o += "    " + d + " = __ddiv_rn(" + a + ", " + b + ");\n"; break;
+      case kPow: o += "    " + d + " = pow(" + a + ", " + b + ");\n"; break;
+      case kMin: o += "    " + d + " = fmin(" + a + ", " + b + ");\n"; break;
+      case kMax: o += "    " + d + " = fmax(" + a + ", " + b + ");\n"; break;
+      default:
+        if (i.op < kNumOps && i.op < sizeof(unary) / sizeof(unary[0]) && unary[i.op])
+          o += "    " + d + " = " + unary[i.op] + "(" + a + ");\n";
+        else
+          o += "    " + d + " = __longlong_as_double(0x7FF8000000000000ll);\n";
+    }
+  }
+  o += "    return s0;\n  }\n};\n";
+  return o;
 }
 
 }  // namespace prog

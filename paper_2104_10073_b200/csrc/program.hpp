@@ -120,5 +120,11 @@ Program compile(const std::string& source, uint32_t dim,
 // shift constants; the tests use the oracle instead.
 double evaluate(const Program& p, const double* x, const double* params);
 
+// CUDA source of `struct <name> { static __device__ double eval(const double*
+// x, const double* p); }` executing the scheduled instruction list as
+// straight-line register code — the interpreter's operations in the
+// interpreter's order (runtime specialisation, csrc/jit.cpp).
+std::string emit_cuda(const Program& p, const std::string& name);
+
 }  // namespace prog
 }  // namespace mcb

@@ -240,3 +240,36 @@ def test_random_programs_vs_oracle(gpu, oracle):
         pts = _oracle.sample_uniform([0.0] * 3, [1.0] * 3, 555, i, 1, 2, 0, n)
         want = np.array([p(row) for row in pts])
         assert _values_close(got, want), src
+
+
+@pytest.mark.gpu
+def test_jit_bit_identical_to_interpreter(gpu, progs):
+    """Runtime-specialised programs (NVRTC, csrc/jit.cpp) against the bytecode
+    interpreter: every per-trial McEstimate byte-identical, in all four modes
+    (direct, unit cube, cells CTA-per-tile, small cells warp-per-tile), for
+    the golden programs incl. non-finite patterns and the random ones."""
+    assert gpu.program_jit(1), gpu.program_jit_error()
+    keep, fns = [], []
+    for i, c in enumerate(progs):
+        params, lo, hi = _case(c)
+        p = gpu.Program(c["source"], c["dim"], list(params))
+        keep.append(p)
+        fns.append(p.integrand(params, low=lo, high=hi, n_samples=min(c["n_samples"], 70_000), index=i))
+    unit = gpu.Program("exp(-3*(x1-0.4)^2) * cos(5*x2) + x3", 3)
+    keep.append(unit)
+    fns.append(unit.integrand(n_samples=100_000, index=len(fns)))          # mode 1
+    cells = unit.integrand(low=[-1, 0, 0], high=[1, 2, 1], n_samples=300_000, index=len(fns) + 1)
+    fns.append(gpu.stratify(cells, cells_per_dim=2))                         # mode 2 (75 000 / cell)
+    fns.append(gpu.stratify(unit.integrand(n_samples=200_000, index=len(fns) + 2)))  # mode 3
+    fns.append(gpu.tree(unit.integrand(n_samples=80_000, index=len(fns) + 3), samples_per_cell=500))
+    n0 = gpu.program_jit_compiles()
+    a = gpu.run_direct(fns, 99, 2)
+    assert gpu.program_jit_error() == "", gpu.program_jit_error()
+    assert gpu.program_jit_compiles() > n0 or os.environ.get("MCB_JIT_CACHE", "") != "0"
+    gpu.program_jit(0)
+    try:
+        b = gpu.run_direct(fns, 99, 2)
+    finally:
+        gpu.program_jit(1)
+    for i in range(len(fns)):
+        assert a[i].tobytes() == b[i].tobytes(), (i, a[i], b[i])
