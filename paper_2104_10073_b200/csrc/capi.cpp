@@ -375,10 +375,12 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
     for (uint32_t j = 0; j < MCB_MAX_DIM; ++j) d.k[j] = f.k[j];
     p.variant = kSafe | (unit_dom ? kUnitDomain : 0) | (strat ? kStrat : 0);
     if (stratified(f) && d.spc <= kWarpTileMaxSpc) p.variant |= kWarpTile;
-    double mid[MCB_MAX_DIM];
-    for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
-    const double c = host_eval(f, mid);
-    d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
+    if (!strat) {  // cells use a per-tile shift computed on the device
+      double mid[MCB_MAX_DIM];
+      for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
+      const double c = host_eval(f, mid);
+      d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
+    }
     return p;
   }
   const bool harm = f.family == MCB_FAMILY_HARMONIC || f.family == MCB_FAMILY_HARMONIC_VEC;
@@ -432,11 +434,14 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   if (strat) p.variant |= kStrat;
   if (tree_cells) p.variant &= ~kNoShift;  // cells shrink: keep the per-tile shift
   if (stratified(f) && d.spc <= kWarpTileMaxSpc) p.variant |= kWarpTile;
-  // shift constant: f at the domain midpoint (reference op order, libm)
-  double mid[MCB_MAX_DIM];
-  for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
-  const double c = host_eval(f, mid);
-  d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
+  // shift constant: f at the domain midpoint (reference op order, libm);
+  // cells use a per-tile shift computed on the device instead
+  if (!strat) {
+    double mid[MCB_MAX_DIM];
+    for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
+    const double c = host_eval(f, mid);
+    d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
+  }
   if (p.variant & kNoShift) d.shift = 0.0;  // the kernel accumulates f itself
   return p;
 }
@@ -771,6 +776,8 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
 mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batches, uint64_t seed,
                           int device) {
   const size_t n = batches.size();
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
   HostPlan hp;
   std::vector<Prepared> prep(n);
   size_t n_rects = 0, n_cells = 0;
@@ -872,6 +879,7 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
     if (g.family != MCB_FAMILY_PROGRAM && !mcb::detail::variant_supported(g.family, g.dim, g.variant))
       return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
   std::memcpy(c.h_descs, hp.descs.data(), sizeof(FnDesc) * n);
+  const auto t_host = clk::now();
   if (n_rects &&
       (e = cudaMemcpyAsync(c.buf.rects, c.h_rects, sizeof(double) * n_rects, cudaMemcpyHostToDevice,
                            c.stream)) != cudaSuccess)
@@ -882,8 +890,18 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
                            cudaMemcpyDeviceToHost, c.stream)) != cudaSuccess)
     return cuda_fail(e, "cudaMemcpyAsync(cell estimates)");
   if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  const auto t_gpu = clk::now();
   for (size_t i = 0; i < n; ++i)
     std::memcpy(batches[i]->est, c.h_cell_est + est_at[i], sizeof(mcb_trial_stats) * batches[i]->n_cells);
+  static const bool trace = [] {
+    const char* env = std::getenv("MCB_TREE_TRACE");
+    return env && *env && *env != '0';
+  }();
+  if (trace) {
+    auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[mcb cells] dev %d: %zu batches, %zu cells: host %.3f ms, H2D+kernels+D2H %.3f ms, scatter %.3f ms\n",
+                 device, n, n_cells, ms(t_start, t_host), ms(t_host, t_gpu), ms(t_gpu, clk::now()));
+  }
   return MCB_OK;
 }
 
