@@ -299,14 +299,37 @@ def run_mcb_arm(args, dist, local):
         "gpu_launches": int(info.launches_per_run) * args.steps,
         "roofline": {"bound": "alu: FP64 pipe (Philox IMAD.WIDE + integrand FP64)",
                      "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "G Philox blocks/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": ncu_traffic(),
+                     "traffic_unit": "DRAM bytes per launch",
                      "blocks_per_launch": blocks_per_launch,
                      "note": "achieved = Philox4x32-10 blocks per launch (2 per 4-D sample) / k_direct "
                              "time; peak = mcb_probe_philox_peak (Philox-only, same code, measured live); "
-                             "DRAM traffic ~0 (ncu: ~180 B per launch, profiles/)"},
+                             "traffic = dram__bytes_read+write of this k_direct launch from " + NCU_SUMMARY +
+                             " (tile table + descriptors; the kernel is ALU-bound)"},
         "clocks": clk.summary(),
     }
     return line
+
+
+NCU_SUMMARY = "profiles/r01_bench_k_direct_ncu_summary.txt"
+
+
+def ncu_traffic():
+    """DRAM bytes (read + write) of one k_direct launch of this bench's
+    workload, from the committed `ncu --set full` summary (None if absent)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), NCU_SUMMARY)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total, found = 0.0, 0
+    try:
+        with open(path) as fh:
+            for line in fh:
+                if "DRAM read (bytes)" in line or "DRAM write (bytes)" in line:
+                    parts = line.split()
+                    total += float(parts[3]) * scale.get(parts[4] if len(parts) > 4 else "byte", 1)
+                    found += 1
+    except OSError:
+        return None
+    return total if found == 2 else None
 
 
 def ctypes_sizeof_integrand():
