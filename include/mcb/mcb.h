@@ -284,6 +284,10 @@ MCB_API mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32
  * returns whether it is active.  Compiled cubins are cached in memory per
  * device and on disk ($MCB_JIT_CACHE, default ~/.cache/mcb-jit; "0" = off). */
 MCB_API int mcb_program_jit(int mode);
+/* Compile a program's specialised kernels without a device (warms the disk
+ * cache ahead of time; MCB_ERR_INVALID_ARGUMENT with the NVRTC log if the
+ * generated code does not compile or NVRTC is missing). */
+MCB_API mcb_status mcb_program_jit_build(const mcb_program* program);
 /* NVRTC compilations so far, and the last JIT failure ("" if none). */
 MCB_API uint64_t mcb_program_jit_compiles(void);
 MCB_API size_t mcb_program_jit_error(char* buf, size_t cap);

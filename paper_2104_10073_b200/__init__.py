@@ -108,7 +108,7 @@ ABI_SYMBOLS = [
     "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
     "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
     "mcb_program_param_name", "mcb_stratified_plan", "mcb_tree_refine", "mcb_program_jit",
-    "mcb_program_jit_compiles", "mcb_program_jit_error",
+    "mcb_program_jit_compiles", "mcb_program_jit_error", "mcb_program_jit_build",
 ]
 
 
@@ -150,6 +150,7 @@ def _load() -> ctypes.CDLL:
         "mcb_program_jit": (i32, [i32]),
         "mcb_program_jit_compiles": (u64, []),
         "mcb_program_jit_error": (sz, [ctypes.c_char_p, sz]),
+        "mcb_program_jit_build": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -236,6 +237,10 @@ class Program:
         f.program = self._h.value
         f.a = f.b = 0.0
         return f
+
+    def jit_build(self) -> None:
+        """NVRTC-compile this program's specialised kernels now (no device needed)."""
+        _check(lib.mcb_program_jit_build(self._h))
 
     def close(self):
         if getattr(self, "_h", None):

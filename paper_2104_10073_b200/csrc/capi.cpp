@@ -1430,6 +1430,13 @@ int mcb_program_jit(int mode) {
 
 uint64_t mcb_program_jit_compiles(void) { return mcb::jit::compile_count(); }
 
+mcb_status mcb_program_jit_build(const mcb_program* program) {
+  if (!program) return fail(MCB_ERR_INVALID_ARGUMENT, "program is NULL");
+  std::string err;
+  if (!mcb::jit::compile_only(program->p, &err)) return fail(MCB_ERR_INVALID_ARGUMENT, "JIT build failed: " + err);
+  return MCB_OK;
+}
+
 size_t mcb_program_jit_error(char* buf, size_t cap) {
   const std::string s = mcb::jit::last_error();
   if (buf && cap) {

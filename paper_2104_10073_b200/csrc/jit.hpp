@@ -47,6 +47,10 @@ bool launch(const prog::Program& p, int mode, uint32_t ctas, const dev::FnDesc* 
 // them one by one on first use.
 void prepare(const std::vector<const prog::Program*>& programs);
 
+// NVRTC-compile `p` (or find it in the disk cache) without a device: warms
+// the on-disk cache ahead of time and checks the generated code.
+bool compile_only(const prog::Program& p, std::string* err);
+
 // Number of NVRTC compilations performed so far (tests / tracing).
 uint64_t compile_count();
 

