@@ -613,7 +613,7 @@ struct DevBuf {
   uint32_t* code = nullptr;
   double* consts = nullptr;
   double* rects = nullptr;              // tree rounds: cell rectangles
-  mcb_trial_stats* cell_est = nullptr;  //   and per-cell estimates
+  mcb::CellEst* cell_est = nullptr;     //   and per-cell estimates
   size_t cap_fns = 0, cap_tiles = 0, cap_part = 0, cap_out = 0, cap_code = 0, cap_consts = 0;
   size_t cap_rects = 0, cap_cell_est = 0;
 
@@ -705,7 +705,7 @@ struct DeviceCtx {
   size_t h_out_cap = 0;
   double* h_rects = nullptr;
   size_t h_rects_cap = 0;
-  mcb_trial_stats* h_cell_est = nullptr;
+  mcb::CellEst* h_cell_est = nullptr;
   size_t h_cell_est_cap = 0;
 };
 
@@ -781,9 +781,14 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
   HostPlan hp;
   std::vector<Prepared> prep(n);
   size_t n_rects = 0, n_cells = 0;
+  std::map<const mcb_integrand*, Prepared> base;  // one prepare per integrand (its trials share it)
   for (size_t i = 0; i < n; ++i) {
     const mcb::tree::CellBatch& b = *batches[i];
-    prep[i] = prepare(*b.fn, seed, uint32_t(b.chunk_base), b.trial, true);
+    auto it = base.find(b.fn);
+    if (it == base.end()) it = base.emplace(b.fn, prepare(*b.fn, seed, 0, 0, true)).first;
+    prep[i] = it->second;
+    prep[i].d.chunk_base = uint32_t(b.chunk_base);
+    prep[i].d.trial_base = b.trial;
     if (b.spc <= mcb::detail::kWarpTileMaxSpc) prep[i].variant |= mcb::detail::kWarpTile;
     n_rects += size_t(b.n_cells) * 2 * b.fn->dim;
     n_cells += b.n_cells;
@@ -886,13 +891,13 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
     return cuda_fail(e, "cudaMemcpyAsync(cells)");
   mcb_status st = enqueue_run(hp, c.buf, 1, c.h_descs, true, c.stream);
   if (st != MCB_OK) return st;
-  if ((e = cudaMemcpyAsync(c.h_cell_est, c.buf.cell_est, sizeof(mcb_trial_stats) * n_cells,
+  if ((e = cudaMemcpyAsync(c.h_cell_est, c.buf.cell_est, sizeof(mcb::CellEst) * n_cells,
                            cudaMemcpyDeviceToHost, c.stream)) != cudaSuccess)
     return cuda_fail(e, "cudaMemcpyAsync(cell estimates)");
   if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   const auto t_gpu = clk::now();
   for (size_t i = 0; i < n; ++i)
-    std::memcpy(batches[i]->est, c.h_cell_est + est_at[i], sizeof(mcb_trial_stats) * batches[i]->n_cells);
+    std::memcpy(batches[i]->est, c.h_cell_est + est_at[i], sizeof(mcb::CellEst) * batches[i]->n_cells);
   static const bool trace = [] {
     const char* env = std::getenv("MCB_TREE_TRACE");
     return env && *env && *env != '0';

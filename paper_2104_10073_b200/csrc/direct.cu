@@ -116,15 +116,9 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
       nn_all += a.nn;
       const double vol = F.cell_rects ? rect_volume(F, c) : cell_volume(F, c);
       if (F.cell_est) {  // tree round: each cell's own direct_mc estimate (reduce_chunks)
-        mcb_trial_stats cs;
-        cs.n_samples = a.n + a.nn;
-        cs.n_nonfinite = a.nn;
+        CellEst cs;
+        cs.n_nonfinite = uint32_t(a.nn);
         cs.status = a.n == 0 ? MCB_TRIAL_ALL_NONFINITE : MCB_TRIAL_OK;
-        cs.nonfinite_warning = double(a.nn) > MCB_NONFINITE_WARN_FRACTION * double(a.n + a.nn) ? 1u : 0u;
-        cs.detail = 0;
-        cs.n_cells = 1;
-        cs.budget_exhausted = 0;
-        cs.max_depth = 0;
         cs.value = a.n == 0 ? 0.0 : __dmul_rn(vol, a.mean);
         cs.std_error = a.n == 0 ? 0.0
                        : a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)),

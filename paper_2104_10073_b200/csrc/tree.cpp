@@ -146,7 +146,7 @@ struct Tree {
   // this round's cells: leaf index, rectangle, estimate; chunk of the first
   std::vector<uint32_t> r_leaf;
   std::vector<double> r_rects;
-  std::vector<mcb_trial_stats> r_est;
+  std::vector<CellEst> r_est;
   uint64_t r_chunk0 = 0;
 
   size_t size() const { return se.size(); }
@@ -228,11 +228,15 @@ mcb_status run_round(std::vector<Tree>& trees, const CellRunner& run, Pool& pool
     for (size_t i = 0; i < t->r_leaf.size(); ++i) {
       const uint32_t l = t->r_leaf[i];
       mcb_trial_stats& e = t->est[l];
-      if (t->r_est[i].status == MCB_TRIAL_OK) {
-        e = t->r_est[i];
+      const CellEst& r = t->r_est[i];
+      if (r.status == MCB_TRIAL_OK) {
+        std::memset(&e, 0, sizeof e);
+        e.value = r.value;
+        e.std_error = r.std_error;
+        e.n_samples = t->spc;
+        e.n_nonfinite = r.n_nonfinite;
+        e.nonfinite_warning = double(r.n_nonfinite) > MCB_NONFINITE_WARN_FRACTION * double(t->spc) ? 1u : 0u;
         e.n_cells = 1;
-        e.budget_exhausted = 0;
-        e.max_depth = 0;
       } else {
         e = dead_leaf(t->spc);
       }

@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "cell_est.hpp"
 #include "mcb/mcb.h"
 
 namespace mcb::tree {
@@ -33,7 +34,7 @@ struct CellBatch {
   uint32_t spc;
   uint32_t n_cells;
   const double* rects;      // n_cells x {low[dim], high[dim]}
-  mcb_trial_stats* est;     // n_cells per-cell estimates (status ALL_NONFINITE = no finite sample)
+  CellEst* est;             // n_cells per-cell estimates (status ALL_NONFINITE = no finite sample)
 };
 
 // Estimates every batch of a round.  Returns MCB_OK or an error status
