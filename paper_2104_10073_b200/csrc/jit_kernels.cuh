@@ -58,6 +58,19 @@ __device__ __forceinline__ void gen_points(const FnDesc& f, const PhiloxPrefix& 
   }
 }
 
+__device__ __forceinline__ void add_pair(const FnDesc& f, uint32_t q, uint32_t count, double f0, double f1,
+                                         double& s1, double& s2, uint32_t& nbad) {
+  const bool has1 = 2 * q + 1 < count;
+  const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
+  nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+  const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
+  const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
+  s1 = __dadd_rn(s1, g0);
+  s2 = fma(g0, g0, s2);
+  s1 = __dadd_rn(s1, g1);
+  s2 = fma(g1, g1, s2);
+}
+
 // Shared pair loop + accumulation: sums of g = f - shift over the finite
 // samples of pairs q = first, first + stride, ... (< pairs).
 template <class P, int D, bool UNIT_DOM>
@@ -67,16 +80,7 @@ __device__ __forceinline__ void accumulate(const FnDesc& f, const PhiloxPrefix& 
   for (uint32_t q = first; q < pairs; q += stride) {
     double x0[D], x1[D];
     gen_points<D, UNIT_DOM>(f, Ph, q, x0, x1);
-    const double f0 = P::eval(x0, params), f1 = P::eval(x1, params);
-    const bool has1 = 2 * q + 1 < count;
-    const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
-    nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
-    const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
-    const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
-    s1 = __dadd_rn(s1, g0);
-    s2 = fma(g0, g0, s2);
-    s1 = __dadd_rn(s1, g1);
-    s2 = fma(g1, g1, s2);
+    add_pair(f, q, count, P::eval(x0, params), P::eval(x1, params), s1, s2, nbad);
   }
 }
 
@@ -179,19 +183,21 @@ __device__ __forceinline__ void tile_warp(const FnDesc* __restrict__ fns, const 
   double params[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) params[i] = f.k[i];
-  {
-    double f0 = 0.0;
-    if (lane == 0) {
-      double x0[D], x1[D];
-      gen_points<D, false>(f, Ph, 0, x0, x1);
-      f0 = P::eval(x0, params);
-      f0 = finite64(f0) ? f0 : 0.0;
-    }
-    f.shift = __shfl_sync(0xFFFFFFFFu, f0, 0);
-  }
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
-  accumulate<P, D, false>(f, Ph, params, lane, 32, pairs, count, s1, s2, nbad);
+  {  // first pair of every lane; lane 0's sample 0 is the per-tile shift
+    double f0 = 0.0, f1 = 0.0;
+    if (lane < pairs) {
+      double x0[D], x1[D];
+      gen_points<D, false>(f, Ph, lane, x0, x1);
+      f0 = P::eval(x0, params);
+      f1 = P::eval(x1, params);
+    }
+    const double c = __shfl_sync(0xFFFFFFFFu, f0, 0);
+    f.shift = finite64(c) ? c : 0.0;
+    if (lane < pairs) add_pair(f, lane, count, f0, f1, s1, s2, nbad);
+  }
+  accumulate<P, D, false>(f, Ph, params, lane + 32, 32, pairs, count, s1, s2, nbad);
   warp_sum(s1, s2, nbad);
   if (lane == 0) {
     TilePartial p;

@@ -207,23 +207,9 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
   dev::cell_rect<D>(f, cell, SAFE ? 1.0 : dev::kTwoM64);
   const uint32_t pairs = (count + 1) >> 1;
   const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
-  if (!NOSHIFT) {  // per-tile shift = f(first sample of the tile), as K3
-    double f0 = 0.0;
-    if (lane == 0) {
-      double st0, st1;
-      dev::gen_pair<FAM, D, false, SAFE>(f, P, 0ull, st0, st1);
-      f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, st0);
-      f0 = finite64(f0) ? f0 : 0.0;
-    }
-    f.shift = __shfl_sync(0xFFFFFFFFu, f0, 0);
-  }
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
-  for (uint32_t q = lane; q < pairs; q += 32) {
-    double x0, x1;
-    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(q * uint32_t(D)), x0, x1);
-    const double f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
-    const double f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
+  auto add = [&](uint32_t q, double f0, double f1) {
     const bool has1 = 2 * q + 1 < count;
     double g0 = NOSHIFT ? f0 : __dsub_rn(f0, f.shift);
     double g1 = NOSHIFT ? f1 : __dsub_rn(f1, f.shift);
@@ -239,6 +225,27 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
     s2 = fma(g0, g0, s2);
     s1 = __dadd_rn(s1, g1);
     s2 = fma(g1, g1, s2);
+  };
+  // First pair of every lane; lane 0's first sample is sample 0 of the tile,
+  // whose value is the per-tile shift (as K3) — broadcast, not re-evaluated.
+  {
+    double f0 = 0.0, f1 = 0.0;
+    if (lane < pairs) {
+      double x0, x1;
+      dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(lane * uint32_t(D)), x0, x1);
+      f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
+      f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
+    }
+    if (!NOSHIFT) {
+      const double c = __shfl_sync(0xFFFFFFFFu, f0, 0);
+      f.shift = finite64(c) ? c : 0.0;
+    }
+    if (lane < pairs) add(lane, f0, f1);
+  }
+  for (uint32_t q = lane + 32; q < pairs; q += 32) {
+    double x0, x1;
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(q * uint32_t(D)), x0, x1);
+    add(q, dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0), dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1));
   }
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) {

@@ -272,22 +272,9 @@ __global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ f
   dev::cell_rect<D>(f, cell, 1.0);
   const uint32_t pairs = (count + 1) >> 1;
   const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
-  {  // per-tile shift = f(first sample of the tile)
-    double f0 = 0.0;
-    if (lane == 0) {
-      gen_points<D, false>(f, P, 0, m.X);
-      interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
-      f0 = m.S[threadIdx.x];
-      f0 = finite64(f0) ? f0 : 0.0;
-    }
-    f.shift = __shfl_sync(0xFFFFFFFFu, f0, 0);
-  }
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
-  for (uint32_t q = lane; q < pairs; q += 32) {
-    gen_points<D, false>(f, P, q, m.X);
-    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
-    const double f0 = m.S[threadIdx.x], f1 = m.S[T + threadIdx.x];
+  auto add = [&](uint32_t q, double f0, double f1) {
     const bool has1 = 2 * q + 1 < count;
     const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
     nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
@@ -297,6 +284,23 @@ __global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ f
     s2 = fma(g0, g0, s2);
     s1 = __dadd_rn(s1, g1);
     s2 = fma(g1, g1, s2);
+  };
+  {  // first pair of every lane; lane 0's sample 0 is the per-tile shift
+    double f0 = 0.0, f1 = 0.0;
+    if (lane < pairs) {
+      gen_points<D, false>(f, P, lane, m.X);
+      interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+      f0 = m.S[threadIdx.x];
+      f1 = m.S[T + threadIdx.x];
+    }
+    const double c = __shfl_sync(0xFFFFFFFFu, f0, 0);
+    f.shift = finite64(c) ? c : 0.0;
+    if (lane < pairs) add(lane, f0, f1);
+  }
+  for (uint32_t q = lane + 32; q < pairs; q += 32) {
+    gen_points<D, false>(f, P, q, m.X);
+    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+    add(q, m.S[threadIdx.x], m.S[T + threadIdx.x]);
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
