@@ -88,14 +88,32 @@ __device__ __forceinline__ void merge_tile(Accum& a, const TilePartial& p) {
   a.n = total;
 }
 
-// K4: ascending-chunk combine per (integrand, trial) and McEstimate fields
-// (reduce_chunks, src/estimator.cpp:55-73).  Stratified integrands: each
-// cell's chunks merge into the cell estimate, cells combine in ascending
-// order (combine_cells, src/estimator.cpp:145-159); a cell without finite
-// samples fails the trial (src/batch.cpp:176-180).
+// K4: one WARP per (integrand, trial).
+//  * direct: lane 0 sums the chunk partials in ascending chunk order and
+//    forms the McEstimate (reduce_chunks, src/estimator.cpp:55-73);
+//  * cell-structured (stratified grid, tree round): lanes take cells
+//    c = lane, lane + 32, ...; each cell's chunks merge (Chan) into the cell's
+//    own direct_mc estimate.  Tree rounds store it per cell; stratified
+//    cells are combined (combine_cells, src/estimator.cpp:145-159) with the
+//    reference's sequential ascending-cell sums (32 cells per step, broadcast
+//    lane by lane); the first dead cell (src/batch.cpp:176-180) is the
+//    minimum over lanes.
+__device__ __forceinline__ mcb_trial_stats cell_estimate(const FnDesc& F, const TilePartial* part, uint64_t base,
+                                                         uint32_t c, Accum& a) {
+  for (uint32_t cc = 0; cc < F.cpc; ++cc) merge_tile(a, part[base + uint64_t(c) * F.cpc + cc]);
+  mcb_trial_stats cs;
+  const double vol = F.cell_rects ? rect_volume(F, c) : cell_volume(F, c);
+  cs.value = a.n == 0 ? 0.0 : __dmul_rn(vol, a.mean);
+  cs.std_error = a.n == 0 ? 0.0
+                 : a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)), double(a.n))))
+                            : __longlong_as_double(0x7FF0000000000000ll);
+  return cs;
+}
+
 __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32_t trials,
                           const TilePartial* __restrict__ part, mcb_trial_stats* __restrict__ out) {
-  const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t idx = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;  // warp-uniform
+  const uint32_t lane = threadIdx.x & 31;
   if (idx >= uint64_t(n_fns) * trials) return;
   const uint32_t fi = uint32_t(idx / trials), t = uint32_t(idx % trials);
   const FnDesc& F = fns[fi];
@@ -107,43 +125,70 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
   st.max_depth = 0;
   if (F.strat_k > 0 || F.cell_rects) {
     double value = 0.0, var = 0.0;
-    uint64_t n_all = 0, nn_all = 0;
-    int dead = -1;
-    for (uint32_t c = 0; c < F.n_cells; ++c) {
-      Accum a;
-      for (uint32_t cc = 0; cc < F.cpc; ++cc) merge_tile(a, part[base + uint64_t(c) * F.cpc + cc]);
-      n_all += a.n + a.nn;
-      nn_all += a.nn;
-      const double vol = F.cell_rects ? rect_volume(F, c) : cell_volume(F, c);
-      if (F.cell_est) {  // tree round: each cell's own direct_mc estimate (reduce_chunks)
-        CellEst cs;
-        cs.n_nonfinite = uint32_t(a.nn);
-        cs.status = a.n == 0 ? MCB_TRIAL_ALL_NONFINITE : MCB_TRIAL_OK;
-        cs.value = a.n == 0 ? 0.0 : __dmul_rn(vol, a.mean);
-        cs.std_error = a.n == 0 ? 0.0
-                       : a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)),
-                                                                          double(a.n))))
-                                  : __longlong_as_double(0x7FF0000000000000ll);
-        F.cell_est[c] = cs;
-        continue;
+    unsigned long long n_all = 0, nn_all = 0;
+    uint32_t dead = 0xFFFFFFFFu;
+    for (uint32_t c0 = 0; c0 < F.n_cells; c0 += 32) {
+      const uint32_t c = c0 + lane;
+      double cv = 0.0, cse2 = 0.0;
+      bool live = false;
+      if (c < F.n_cells) {
+        Accum a;
+        const mcb_trial_stats cs = cell_estimate(F, part, base, c, a);
+        n_all += a.n + a.nn;
+        nn_all += a.nn;
+        if (F.cell_est) {  // tree round: the cell's own estimate
+          CellEst ce;
+          ce.value = cs.value;
+          ce.std_error = cs.std_error;
+          ce.n_nonfinite = uint32_t(a.nn);
+          ce.status = a.n == 0 ? MCB_TRIAL_ALL_NONFINITE : MCB_TRIAL_OK;
+          F.cell_est[c] = ce;
+        } else if (a.n == 0) {
+          dead = min(dead, c);
+        } else {
+          cv = cs.value;
+          cse2 = __dmul_rn(cs.std_error, cs.std_error);
+          live = true;
+        }
       }
-      if (a.n == 0) {
-        if (dead < 0) dead = int(c);
-        continue;
+      if (F.cell_est) continue;
+      // combine_cells order: the running sums take the cells one by one in
+      // ascending order (broadcast from their lanes), exactly as the reference
+      const uint32_t live_mask = __ballot_sync(0xFFFFFFFFu, live);
+      for (int i = 0; i < 32; ++i) {
+        const double v = __shfl_sync(0xFFFFFFFFu, cv, i);
+        const double w = __shfl_sync(0xFFFFFFFFu, cse2, i);
+        if (live_mask & (1u << i)) {
+          value = __dadd_rn(value, v);
+          var = __dadd_rn(var, w);
+        }
       }
-      value = __dadd_rn(value, __dmul_rn(vol, a.mean));
-      const double se = a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)),
-                                                                         double(a.n))))
-                                 : __longlong_as_double(0x7FF0000000000000ll);
-      var = __dadd_rn(var, __dmul_rn(se, se));
     }
+    if (F.cell_est) {
+      if (lane == 0) {
+        st.status = MCB_TRIAL_OK;
+        st.value = st.std_error = 0.0;
+        st.n_samples = st.n_nonfinite = 0;
+        st.nonfinite_warning = 0;
+        st.n_cells = F.n_cells;
+        out[F.out_slot * trials + t] = st;
+      }
+      return;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      n_all += __shfl_xor_sync(0xFFFFFFFFu, n_all, m);
+      nn_all += __shfl_xor_sync(0xFFFFFFFFu, nn_all, m);
+    }
+    dead = __reduce_min_sync(0xFFFFFFFFu, dead);
+    if (lane != 0) return;
     st.n_cells = F.n_cells;
     st.n_samples = n_all;
     st.n_nonfinite = nn_all;
     st.nonfinite_warning = double(nn_all) > MCB_NONFINITE_WARN_FRACTION * double(n_all) ? 1u : 0u;
-    if (dead >= 0) {
+    if (dead != 0xFFFFFFFFu) {
       st.status = MCB_TRIAL_DEAD_CELL;
-      st.detail = uint32_t(dead);
+      st.detail = dead;
       st.value = 0.0;
       st.std_error = 0.0;
     } else {
@@ -154,6 +199,7 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
     out[F.out_slot * trials + t] = st;
     return;
   }
+  if (lane != 0) return;
   double s1 = 0.0, s2 = 0.0;
   uint64_t n = 0, nb = 0;
   for (uint32_t c = 0; c < F.n_chunks; ++c) {
@@ -285,7 +331,7 @@ cudaError_t launch_combine(const FnDesc* fns, uint32_t n_fns, uint32_t trials,
                            const TilePartial* part, mcb_trial_stats* out, cudaStream_t s) {
   const uint64_t n = uint64_t(n_fns) * trials;
   if (n == 0) return cudaSuccess;
-  k_combine<<<uint32_t((n + 127) / 128), 128, 0, s>>>(fns, n_fns, trials, part, out);
+  k_combine<<<uint32_t((n + 3) / 4), 128, 0, s>>>(fns, n_fns, trials, part, out);  // a warp per (fn, trial)
   return cudaGetLastError();
 }
 

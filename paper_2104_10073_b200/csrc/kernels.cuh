@@ -242,7 +242,21 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
     }
     if (lane < pairs) add(lane, f0, f1);
   }
-  for (uint32_t q = lane + 32; q < pairs; q += 32) {
+  // two pairs per iteration (q, q + 32): independent Philox / trig chains
+  // interleave, as K3's software pipeline does; sums keep ascending q order
+  uint32_t q = lane + 32;
+  for (; q + 32 < pairs; q += 64) {
+    double x0, x1, y0, y1;
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(q * uint32_t(D)), x0, x1);
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t((q + 32) * uint32_t(D)), y0, y1);
+    const double a0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
+    const double a1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
+    const double b0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, y0);
+    const double b1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, y1);
+    add(q, a0, a1);
+    add(q + 32, b0, b1);
+  }
+  if (q < pairs) {
     double x0, x1;
     dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(q * uint32_t(D)), x0, x1);
     add(q, dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0), dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1));
