@@ -177,8 +177,15 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
 // tile start to finish: per-warp shift (lane 0, broadcast), lane-strided
 // pairs, warp butterfly, one TilePartial per tile — no CTA barrier after the
 // table.  Same sums per tile as K3 up to the (fixed) reduction shape.
+// Resident CTAs per SM of k_direct_warp: the warp-per-tile loop is latency-
+// bound, so occupancy pays as long as nothing spills (ptxas -v: 64 registers
+// suffice up to 4-D, 80 up to 6-D; SAFE calls libdevice sincos).
+constexpr int warp_tile_min_blocks(int D, int V) {
+  return (V & kSafe) ? 2 : (D <= 4 ? 4 : (D <= 6 ? 3 : 2));
+}
+
 template <int FAM, int D, int V>
-__global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
     k_direct_warp(const FnDesc* __restrict__ fns, const uint32_t* __restrict__ tile_fn, uint64_t tile0,
                   TilePartial* __restrict__ part) {
   constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
