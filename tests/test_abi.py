@@ -115,3 +115,33 @@ def test_validation_error_precedes_device_check(mcb):
     with pytest.raises(mcb.McbError) as e:
         mcb.run_direct([mcb.harmonic(2.0, 2, n_samples=1)], 1, 2)
     assert e.value.status == 2 and "samples must be >= 2" in str(e.value)
+
+
+def test_validate_edges(mcb):
+    """Sizes and descriptors at and past the supported limits."""
+    f9 = mcb.harmonic(1.0, 8, n_samples=100)
+    f9.dim = 9
+    assert (0, "dim 9 exceeds the supported maximum 8") in mcb.validate([f9], 1)
+    f0 = mcb.harmonic(1.0, 1, n_samples=100)
+    f0.dim = 0
+    assert (0, "dim must be >= 1") in mcb.validate([f0], 1)
+    huge = mcb.harmonic(1.0, 2, n_samples=(2**32 + 1) * 65536)
+    assert (0, "samples exceed 2^32 chunks (chunk_index is 32-bit)") in mcb.validate([huge], 1)
+    many = mcb.harmonic(1.0, 2, n_samples=2**20 * 65536)
+    assert (0, "chunks x trials exceeds 2^32 work units for one integrand") in mcb.validate([many], 2**13)
+    nan_dom = mcb.harmonic(1.0, 2, low=[0.0, float("nan")], high=[1.0, 1.0], n_samples=100)
+    inf_dom = mcb.harmonic(1.0, 2, low=[0.0, 0.0], high=[1.0, float("inf")], n_samples=100)
+    msg = "domain is invalid (need low[i] < high[i], finite, dim >= 1)"
+    assert (0, msg) in mcb.validate([nan_dom], 1) and (0, msg) in mcb.validate([inf_dom], 1)
+    fam = mcb.harmonic(1.0, 2, n_samples=100)
+    fam.family = 9
+    assert (0, "unknown integrand family 9") in mcb.validate([fam], 1)
+    flg = mcb.harmonic(1.0, 2, n_samples=100)
+    flg.flags |= 0x80
+    assert (0, "unknown flag bits") in mcb.validate([flg], 1)
+    unit = mcb.harmonic(1.0, 2, a=2.0, b=1.0, n_samples=100)
+    unit.flags = mcb.FLAG_UNIT_COEFFS
+    assert (0, "unit-coefficient flag needs the harmonic family with a = b = 1") in mcb.validate([unit], 1)
+    prog = mcb.make_integrand(mcb.FAMILY_PROGRAM, 2, n_samples=100)
+    assert (0, "program family needs a compiled program") in mcb.validate([prog], 1)
+    assert mcb.validate([mcb.harmonic(1.0, 8, n_samples=2)], 1) == []  # the minimum budget

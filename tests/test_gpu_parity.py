@@ -286,3 +286,21 @@ def test_acceptance_c2_eq2_oracles(gpu):
     out = gpu.run_direct([a, b], 2026, 1)
     assert abs(out[0, 0]["value"] - 1.0) <= 3 * out[0, 0]["std_error"]
     assert abs(out[1, 0]["value"] - 7.0 / 12.0) <= 3 * out[1, 0]["std_error"]
+
+
+@pytest.mark.gpu
+def test_chunk_boundary_counts_vs_oracle(gpu):
+    """Sample counts at the chunk and pair boundaries (2, odd, 65535..65537,
+    2 chunks +- 1) in odd and even dimensions, one trial (trial stddev 0)."""
+    fns = []
+    for n in (2, 3, 65535, 65536, 65537, 131071, 131072, 131073):
+        for d in (1, 3, 7, 8):
+            fns.append(gpu.harmonic(3.0 + d, d, a=0.7, b=-1.3, low=[-0.5] * d, high=[0.25 + 0.1 * d] * d,
+                                    n_samples=n, index=len(fns)))
+    out = gpu.run_direct(fns, 31337, 1)
+    ref = _oracle.run_direct(fns, 31337, 1)
+    for i, f in enumerate(fns):
+        check_stats(out[i, 0], float(ref[i, 0]["value"]), float(ref[i, 0]["std_error"]),
+                    int(ref[i, 0]["n_samples"]), int(ref[i, 0]["n_nonfinite"]), 2.0 * gpu.volume(f) * 10)
+        mean, sd, n_ok = gpu.summarize_trials(out[i])
+        assert n_ok == 1 and sd == 0.0 and mean == float(out[i, 0]["value"])
