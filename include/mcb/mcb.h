@@ -242,6 +242,17 @@ MCB_API mcb_status mcb_tree_refine(const mcb_integrand* fn, uint64_t seed, uint3
                                    uint64_t chunk_base, int device, mcb_trial_stats* out,
                                    mcb_leaf* leaves, size_t leaf_cap, size_t* n_leaves);
 
+/* stratified_mc (src/estimator.cpp:161-182): `cells_per_dim`^d grid cells
+ * (at most `cell_cap`; 0 = 1e6), direct_mc of `samples_per_cell` samples per
+ * cell with chunk keys chunk_base + c * chunk_count(samples_per_cell),
+ * combine_cells.  Leaves as in mcb_tree_refine.  A cell without a finite
+ * sample fails the call as in the reference (out->status MCB_TRIAL_DEAD_CELL,
+ * detail = the cell); a grid past the cap gives MCB_TRIAL_CELL_BUDGET. */
+MCB_API mcb_status mcb_stratified_mc(const mcb_integrand* fn, uint32_t cells_per_dim, uint32_t samples_per_cell,
+                                     uint64_t cell_cap, uint64_t seed, uint32_t trial, uint64_t chunk_base,
+                                     int device, mcb_trial_stats* out, mcb_leaf* leaves, size_t leaf_cap,
+                                     size_t* n_leaves);
+
 /* ---- device-resident plans (descriptors stay in HBM; async on a stream) -- */
 typedef struct mcb_plan mcb_plan;
 typedef struct mcb_plan_info {

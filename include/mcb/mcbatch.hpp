@@ -208,6 +208,22 @@ struct CellBudgetExceeded : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// src/estimator.cpp:161-182: cells_per_dim^d grid cells of samples_per_cell
+// samples, combine_cells; throws AllSamplesNonFinite for a cell without a
+// finite sample, CellBudgetExceeded past cell_cap.
+std::pair<McEstimate, std::vector<StratumNode>> stratified_mc(const IntegrandSpec& spec,
+                                                              std::uint32_t cells_per_dim,
+                                                              std::uint32_t samples_per_cell,
+                                                              const StreamKey& key_base,
+                                                              std::uint64_t cell_cap = 1000000,
+                                                              int device = 0);
+
+// Host helpers of the cell methods (src/estimator.cpp:94-159).
+std::uint64_t cell_grid_size(std::uint32_t cells_per_dim, std::size_t dim, std::uint64_t cap);  // throws
+std::uint32_t auto_cells_per_dim(std::size_t dim, std::uint64_t cell_limit);
+HyperRect grid_cell(const HyperRect& rect, std::uint32_t cells_per_dim, std::uint64_t index);
+McEstimate combine_cells(std::span<const McEstimate> cells);
+
 // src/estimator.cpp:212-318 with the config's total_budget; cells estimated on
 // `device`.  Throws AllSamplesNonFinite / CellBudgetExceeded like the reference.
 McEstimate tree_refine(const IntegrandSpec& spec, const RefineConfig& config, const StreamKey& key_base,

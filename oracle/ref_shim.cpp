@@ -311,6 +311,49 @@ int ref_tree_refine_source(const char* source, const mcb_integrand* f, const cha
   }
 }
 
+// stratified_mc (src/estimator.cpp:161-182) of an arbitrary source; leaves
+// (cap entries) in grid order.  A dead cell gives status DEAD_CELL.
+int ref_stratified_mc_source(const char* source, const mcb_integrand* f, const char* const* names,
+                             const double* values, std::size_t n_params, std::uint32_t cells_per_dim,
+                             std::uint32_t samples_per_cell, std::uint64_t cell_cap, std::uint64_t seed,
+                             std::uint32_t trial, std::uint64_t chunk_base, mcb_trial_stats* out,
+                             mcb_leaf* leaves, std::size_t cap, std::size_t* n_leaves) {
+  try {
+    std::map<std::string, double> pm;
+    for (std::size_t i = 0; i < n_params; ++i) pm[names[i]] = values[i];
+    std::vector<std::string> nm;
+    std::vector<double> vals;
+    for (auto& [k, v] : pm) { nm.push_back(k); vals.push_back(v); }
+    CompiledProgram prog = compile(parse(source), f->dim, nm);
+    std::memset(out, 0, sizeof *out);
+    if (n_leaves) *n_leaves = 0;
+    try {
+      auto [est, lv] = stratified_mc(prog, vals, rect_of(f->dim, f->low, f->high), cells_per_dim,
+                                     samples_per_cell, StreamKey{seed, f->integrand_index, trial, chunk_base},
+                                     cell_cap ? cell_cap : 1000000);
+      fill(est, out);
+      out->n_cells = std::uint32_t(lv.size());
+      if (n_leaves) *n_leaves = lv.size();
+      for (std::size_t i = 0; i < lv.size() && i < cap; ++i) {
+        std::memset(&leaves[i], 0, sizeof leaves[i]);
+        for (std::uint32_t j = 0; j < f->dim; ++j) {
+          leaves[i].low[j] = lv[i].cell.low[j];
+          leaves[i].high[j] = lv[i].cell.high[j];
+        }
+        fill(lv[i].estimate, &leaves[i].estimate);
+      }
+    } catch (const AllSamplesNonFinite&) {
+      out->status = MCB_TRIAL_DEAD_CELL;
+    } catch (const CellBudgetExceeded&) {
+      out->status = MCB_TRIAL_CELL_BUDGET;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // read_job + write_job (src/job_io.cpp:114-142): re-serialise a job file.
 int ref_job_roundtrip(const char* in_path, const char* out_path) {
   try {

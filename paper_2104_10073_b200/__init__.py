@@ -108,7 +108,7 @@ ABI_SYMBOLS = [
     "mcb_plan_get_info", "mcb_plan_destroy", "mcb_debug_points", "mcb_debug_eval",
     "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
     "mcb_program_param_name", "mcb_stratified_plan", "mcb_tree_refine", "mcb_program_jit",
-    "mcb_program_jit_compiles", "mcb_program_jit_error", "mcb_program_jit_build",
+    "mcb_program_jit_compiles", "mcb_program_jit_error", "mcb_program_jit_build", "mcb_stratified_mc",
 ]
 
 
@@ -151,6 +151,8 @@ def _load() -> ctypes.CDLL:
         "mcb_program_jit_compiles": (u64, []),
         "mcb_program_jit_error": (sz, [ctypes.c_char_p, sz]),
         "mcb_program_jit_build": (i32, [vp]),
+        "mcb_stratified_mc": (i32, [P(Integrand), u32, u32, u64, u64, u32, u64, i32, P(TrialStats), P(Leaf), sz,
+                                    P(sz)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -370,6 +372,19 @@ def tree_refine(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, de
     buf = (Leaf * max(1, n.value))()
     _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), buf,
                                n.value, ctypes.byref(n)))
+    return st, list(buf[:n.value])
+
+
+def stratified_mc(f: Integrand, cells_per_dim: int, samples_per_cell: int, seed: int, trial: int = 0,
+                  chunk_base: int = 0, cell_cap: int = 0, device: int = 0):
+    """stratified_mc (ref src/estimator.cpp:161-182) on the GPU: (TrialStats, [Leaf])."""
+    st = TrialStats()
+    n = ctypes.c_size_t()
+    _check(lib.mcb_stratified_mc(ctypes.byref(f), cells_per_dim, samples_per_cell, cell_cap, seed, trial,
+                                 chunk_base, device, ctypes.byref(st), None, 0, ctypes.byref(n)))
+    buf = (Leaf * max(1, n.value))()
+    _check(lib.mcb_stratified_mc(ctypes.byref(f), cells_per_dim, samples_per_cell, cell_cap, seed, trial,
+                                 chunk_base, device, ctypes.byref(st), buf, n.value, ctypes.byref(n)))
     return st, list(buf[:n.value])
 
 

@@ -6,6 +6,7 @@
 //   mcb_run_direct      run_batch (Direct)       src/batch.cpp:195-333
 //   mcb_direct_mc       direct_mc                src/estimator.cpp:75-92
 //   mcb_tree_refine     tree_refine              src/estimator.cpp:212-318 (tree.cpp)
+//   mcb_stratified_mc   stratified_mc            src/estimator.cpp:161-182
 //   mcb_summarize_trials summarize_trials        src/estimator.cpp:320-337
 //   mcb_stream_key      UniformStream key        src/sampling.cpp:84-87
 //   mcb_volume          HyperRect::volume        src/sampling.cpp:16-20
@@ -1308,6 +1309,49 @@ mcb_status mcb_tree_refine(const mcb_integrand* fn, uint64_t seed, uint32_t tria
   if (n_leaves) *n_leaves = lv.size();
   if (leaves)
     std::memcpy(leaves, lv.data(), sizeof(mcb_leaf) * std::min(leaf_cap, lv.size()));
+  return MCB_OK;
+}
+
+mcb_status mcb_stratified_mc(const mcb_integrand* fn, uint32_t cells_per_dim, uint32_t samples_per_cell,
+                             uint64_t cell_cap, uint64_t seed, uint32_t trial, uint64_t chunk_base, int device,
+                             mcb_trial_stats* out, mcb_leaf* leaves, size_t leaf_cap, size_t* n_leaves) {
+  if (!fn || !out) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (cells_per_dim == 0) return fail(MCB_ERR_INVALID_ARGUMENT, "cells_per_dim must be >= 1");
+  if (samples_per_cell < 2) return fail(MCB_ERR_INVALID_ARGUMENT, "n_samples must be >= 2");
+  mcb_integrand f = *fn;
+  f.method = MCB_METHOD_DIRECT;
+  mcb_status st = validate_for_run(&f, 1, 1);
+  if (st != MCB_OK) return st;
+  if ((st = check_device(device)) != MCB_OK) return st;
+  // = the first pass of tree_refine with the grid given and no refinement
+  f.method = MCB_METHOD_TREE;
+  f.flags |= MCB_FLAG_REFINE_CONFIG;
+  f.cells_per_dim = cells_per_dim;
+  f.samples_per_cell = samples_per_cell;
+  f.max_depth = 0;
+  f.cell_cap = cell_cap;
+  std::vector<mcb_leaf> lv;
+  std::vector<mcb::tree::TreeTask> tasks{mcb::tree::TreeTask{&f, trial, chunk_base, out, &lv}};
+  const std::vector<int> devs{device};
+  st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
+    return run_cells(batches, seed, devs);
+  });
+  if (st != MCB_OK) return st;
+  if (out->status == MCB_TRIAL_ALL_NONFINITE) {  // every cell dead: the first one throws
+    out->status = MCB_TRIAL_DEAD_CELL;
+    out->detail = 0;
+  } else if (out->status == MCB_TRIAL_OK) {
+    for (size_t i = 0; i < lv.size(); ++i)
+      if (lv[i].estimate.status != MCB_TRIAL_OK) {  // direct_mc of cell i threw
+        out->status = MCB_TRIAL_DEAD_CELL;
+        out->detail = uint32_t(i);
+        out->value = out->std_error = 0.0;
+        lv.clear();
+        break;
+      }
+  }
+  if (n_leaves) *n_leaves = lv.size();
+  if (leaves) std::memcpy(leaves, lv.data(), sizeof(mcb_leaf) * std::min(leaf_cap, lv.size()));
   return MCB_OK;
 }
 

@@ -380,6 +380,96 @@ McEstimate tree_refine(const IntegrandSpec& spec, const RefineConfig& config, co
   return to_estimate(st);
 }
 
+std::pair<McEstimate, std::vector<StratumNode>> stratified_mc(const IntegrandSpec& spec,
+                                                              std::uint32_t cells_per_dim,
+                                                              std::uint32_t samples_per_cell,
+                                                              const StreamKey& key_base, std::uint64_t cell_cap,
+                                                              int device) {  // :161-182
+  if (spec.domain.dim() != spec.dim) throw std::invalid_argument("program/domain dimension mismatch");
+  if (cells_per_dim == 0) throw std::invalid_argument("cells_per_dim must be >= 1");
+  IntegrandSpec s = spec;
+  s.method = Method::Direct;
+  ProgramCache programs;
+  const mcb_program* prog = s.family == Family::Program ? programs.get(s) : nullptr;
+  mcb_integrand d = to_descriptor(s, key_base.integrand_index, prog);
+  mcb_trial_stats st{};
+  size_t n = 0;
+  check(mcb_stratified_mc(&d, cells_per_dim, samples_per_cell, cell_cap, key_base.global_seed,
+                          key_base.trial_index, key_base.chunk_index, device, &st, nullptr, 0, &n));
+  std::vector<mcb_leaf> lv(n);
+  if (n)
+    check(mcb_stratified_mc(&d, cells_per_dim, samples_per_cell, cell_cap, key_base.global_seed,
+                            key_base.trial_index, key_base.chunk_index, device, &st, lv.data(), lv.size(), &n));
+  if (st.status == MCB_TRIAL_CELL_BUDGET) throw CellBudgetExceeded("cell grid exceeds configured cap");
+  if (st.status == MCB_TRIAL_CHUNK_RANGE) throw std::out_of_range("chunk_index exceeds 32 bits");
+  if (st.status != MCB_TRIAL_OK) throw AllSamplesNonFinite("every sample evaluated to NaN or infinity");
+  std::vector<StratumNode> leaves;
+  leaves.reserve(lv.size());
+  for (const mcb_leaf& l : lv) {
+    StratumNode node;
+    node.cell.low.assign(l.low, l.low + s.dim);
+    node.cell.high.assign(l.high, l.high + s.dim);
+    node.estimate = to_estimate(l.estimate);
+    node.depth = l.depth;
+    leaves.push_back(std::move(node));
+  }
+  return {to_estimate(st), std::move(leaves)};
+}
+
+std::uint64_t cell_grid_size(std::uint32_t k, std::size_t dim, std::uint64_t cap) {  // :94-105
+  if (k == 0) throw std::invalid_argument("cells_per_dim must be >= 1");
+  std::uint64_t cells = 1;
+  for (std::size_t i = 0; i < dim; ++i) {
+    if (cells > cap / k + 1) throw CellBudgetExceeded("cell grid exceeds configured cap");
+    cells *= k;
+  }
+  if (cells > cap) throw CellBudgetExceeded("cell grid exceeds configured cap");
+  return cells;
+}
+
+std::uint32_t auto_cells_per_dim(std::size_t dim, std::uint64_t limit) {  // :107-122
+  std::uint32_t k = 1;
+  for (;;) {
+    std::uint64_t cells = 1;
+    for (std::size_t i = 0; i < dim; ++i) {
+      cells *= std::uint64_t(k) + 1;
+      if (cells > limit) return k;
+    }
+    ++k;
+  }
+}
+
+HyperRect grid_cell(const HyperRect& rect, std::uint32_t k, std::uint64_t index) {  // :124-143
+  const std::size_t d = rect.dim();
+  HyperRect cell;
+  cell.low.resize(d);
+  cell.high.resize(d);
+  std::uint64_t rem = index;
+  for (std::size_t j = d; j-- > 0;) {  // axis 0 is the most significant digit
+    const std::uint32_t digit = std::uint32_t(rem % k);
+    rem /= k;
+    const double width = rect.high[j] - rect.low[j];
+    cell.low[j] = digit == 0 ? rect.low[j] : rect.low[j] + width * (double(digit) / k);
+    cell.high[j] = digit + 1 == k ? rect.high[j] : rect.low[j] + width * (double(digit + 1) / k);
+  }
+  return cell;
+}
+
+McEstimate combine_cells(std::span<const McEstimate> cells) {  // :145-159
+  McEstimate total;
+  double var = 0.0;
+  for (const McEstimate& c : cells) {
+    total.value += c.value;
+    var += c.std_error * c.std_error;
+    total.n_samples += c.n_samples;
+    total.n_nonfinite += c.n_nonfinite;
+    total.budget_exhausted |= c.budget_exhausted;
+  }
+  total.std_error = std::sqrt(var);
+  total.nonfinite_warning = double(total.n_nonfinite) > kNonFiniteWarnFraction * double(total.n_samples);
+  return total;
+}
+
 TrialSummary summarize_trials(std::vector<McEstimate> per_trial) {  // :320-337
   TrialSummary s;
   s.per_trial = std::move(per_trial);

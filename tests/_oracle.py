@@ -140,6 +140,26 @@ def ref_tree_refine(source, f, params, seed, trial=0, chunk_base=0):
     return st, list(buf[:min(n.value, cap)])
 
 
+def ref_stratified_mc(source, f, params, cells_per_dim, spc, seed, trial=0, chunk_base=0, cell_cap=0):
+    """The reference's own stratified_mc of `source` (params: name -> value)."""
+    from paper_2104_10073_b200 import Leaf, TrialStats
+    lib = load_ref()
+    if lib is None:
+        raise FileNotFoundError(REF_SO)
+    names = list(params)
+    cn = (ctypes.c_char_p * max(1, len(names)))(*[n.encode() for n in names])
+    cv = (ctypes.c_double * max(1, len(names)))(*[params[n] for n in names])
+    st = TrialStats()
+    n = ctypes.c_size_t()
+    cap = 1 << 16
+    buf = (Leaf * cap)()
+    if lib.ref_stratified_mc_source(source.encode(), ctypes.byref(f), cn, cv, len(names), cells_per_dim, spc,
+                                    cell_cap, seed, trial, chunk_base, ctypes.byref(st), buf, cap,
+                                    ctypes.byref(n)) != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return st, list(buf[:min(n.value, cap)])
+
+
 def direct_mc(f, seed, trial=0, chunk_base=0):
     from paper_2104_10073_b200 import TrialStats
     lib = load()
@@ -193,6 +213,8 @@ def load_ref():
         "ref_job_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
         "ref_results_roundtrip": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
         "ref_run_command": (i32, [ctypes.c_char_p, ctypes.c_char_p, i32]),
+        "ref_stratified_mc_source": (i32, [ctypes.c_char_p, P(Integrand), P(ctypes.c_char_p), P(dbl), sz, u32, u32,
+                                           u64, u64, u32, u64, P(TrialStats), P(Leaf), sz, P(sz)]),
         "ref_tree_refine_source": (i32, [ctypes.c_char_p, P(Integrand), P(ctypes.c_char_p), P(dbl), sz, u64,
                                          u32, u64, P(TrialStats), P(Leaf), sz, P(sz)]),
     }

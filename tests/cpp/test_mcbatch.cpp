@@ -407,9 +407,38 @@ static void tree_cases() {
   }
 }
 
+// tests/test_estimator.cpp:87-138 — stratified_mc and the cell helpers
+static void stratified_cases() {
+  IntegrandSpec f = IntegrandSpec::from_source("s", "sin(x1)*x2", 2, HyperRect::box({0.25, -1.0}, {0.75, 3.0}),
+                                               {}, 5000);
+  auto [one, leaves1] = stratified_mc(f, 1, 5000, StreamKey{11, 2, 0, 0});
+  McEstimate d = direct_mc(f, 5000, StreamKey{11, 2, 0, 0});
+  CHECK(leaves1.size() == 1);
+  CHECK(std::fabs(one.value - d.value) <= 1e-13 * std::fabs(d.value));  // 1x1 cells = direct_mc
+  auto [est, leaves] = stratified_mc(f, 4, 200, StreamKey{3, 0, 0, 0});
+  CHECK(leaves.size() == 16);
+  double vol = 0.0;
+  for (const StratumNode& n : leaves) vol += n.cell.volume();
+  CHECK(std::fabs(vol - 2.0) <= 1e-12);
+  CHECK(est.n_samples == 16 * 200);
+  CHECK(cell_grid_size(4, 2, 1000000) == 16);
+  CHECK_THROWS_AS(cell_grid_size(10, 7, 1000000), CellBudgetExceeded);
+  CHECK(auto_cells_per_dim(4, 4096) == 8);
+  const HyperRect c = grid_cell(HyperRect::box({0.25, -1.0}, {0.75, 3.0}), 4, 5);
+  CHECK(c.low == leaves[5].cell.low && c.high == leaves[5].cell.high);
+  std::vector<McEstimate> cells;
+  for (const StratumNode& n : leaves) cells.push_back(n.estimate);
+  const McEstimate comb = combine_cells(cells);
+  CHECK(comb.value == est.value && comb.std_error == est.std_error);
+  IntegrandSpec lg = IntegrandSpec::from_source("l", "log(x1)", 1, HyperRect::box({-1.0}, {1.0}), {}, 4000);
+  CHECK_THROWS_AS(stratified_mc(lg, 4, 1000, StreamKey{9, 0, 0, 0}), AllSamplesNonFinite);
+  CHECK_THROWS_AS(stratified_mc(f, 10, 10, StreamKey{3, 0, 0, 0}, 50), CellBudgetExceeded);
+}
+
 int main() {
   constants_are_exact();
   tree_cases();
+  stratified_cases();
   mixed_dimension_batch();
   validate_reports_every_violation();
   device_invariance();

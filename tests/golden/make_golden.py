@@ -172,6 +172,9 @@ def main():
     # leaves, and run_batch's Tree branch (src/batch.cpp:276-289)
     g["tree"] = make_tree_goldens(ref)
 
+    # 9. stratified_mc standalone (src/estimator.cpp:161-182) with leaves
+    g["stratified_mc"] = make_stratified_mc_goldens()
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(g, fh, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))
@@ -316,6 +319,33 @@ def make_tree_goldens(ref):
               "mean": H(float(mean[i])), "trial_stddev": H(float(sd[i])), "ok": int(ok[i])}
              for i, f in enumerate(fns)]
     return {"cases": out, "batch": {"seed": 77, "trials": 3, "cases": batch}}
+
+
+STRAT_MC_CASES = [
+    # (source, dim, params, low, high, cells_per_dim, spc, seed, index, trial, chunk_base, cell_cap)
+    ("sin(x1)*x2", 2, {}, [0.25, -1.0], [0.75, 3.0], 1, 5000, 11, 2, 0, 0, 0),   # test_estimator.cpp:87-97
+    ("exp(-a*((x1-0.5)^2+(x2-0.3)^2)) + x1*x2", 2, {"a": 20.0}, [0, 0], [1, 1], 3, 333, 123, 5, 0, 0, 0),
+    ("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, {"k": 13.0}, [0] * 4, [1] * 4, 3, 700, 9, 1, 2, 5, 0),
+    ("5", 3, {}, [0, 0, 0], [2, 1, 1], 4, 100, 1, 0, 0, 0, 0),
+    ("log(x1)", 1, {}, [-1], [1], 4, 1000, 9, 0, 0, 0, 0),                        # dead cells
+    ("x1", 2, {}, [0, 0], [1, 1], 10, 10, 3, 0, 0, 0, 50),                        # past the cap
+    ("abs(x1-x2)*x3", 3, {}, [-1, 0, 0], [1, 1, 2], 2, 70_000, 4, 3, 1, 0, 0),    # 2-chunk cells
+]
+
+
+def make_stratified_mc_goldens():
+    out = []
+    for src, dim, params, lo, hi, k, spc, seed, index, trial, cb, cap in STRAT_MC_CASES:
+        prog = mcb.Program(src, dim, list(params))
+        f = prog.integrand(params, low=lo, high=hi, n_samples=max(2, spc), index=index)
+        st, leaves = _oracle.ref_stratified_mc(src, f, params, k, spc, seed, trial, cb, cap)
+        out.append({"source": src, "dim": dim, "params": {kk: H(float(x)) for kk, x in params.items()},
+                    "low": [H(float(x)) for x in lo], "high": [H(float(x)) for x in hi], "cells_per_dim": k,
+                    "samples_per_cell": spc, "seed": seed, "index": index, "trial": trial, "chunk_base": cb,
+                    "cell_cap": cap, "estimate": dict(stats_json(st), n_leaves=len(leaves)),
+                    "leaves": [[[H(l.low[j]) for j in range(dim)], [H(l.high[j]) for j in range(dim)],
+                                H(l.estimate.value), H(l.estimate.std_error)] for l in leaves]})
+    return out
 
 
 def _as_stats(row):

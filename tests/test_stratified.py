@@ -146,3 +146,36 @@ def test_stratified_device_invariance(gpu):
         gpu.stratify(f)
     runs = [gpu.run_direct(fns, 5, 2, devices=d) for d in ([0], [0, 0], [0, 0, 0, 0])]
     assert runs[0].tobytes() == runs[1].tobytes() == runs[2].tobytes()
+
+
+@pytest.mark.gpu
+def test_stratified_mc_vs_reference_golden(gpu):
+    """stratified_mc standalone (ref src/estimator.cpp:161-182) with leaves:
+    grid rectangles bit-exact, cell and total estimates to rounding, dead
+    cells and the cell cap fail as in the reference."""
+    with open(GOLDEN) as fh:
+        cases = json.load(fh)["stratified_mc"]
+    for c in cases:
+        params = {k: fx(v) for k, v in c["params"].items()}
+        prog = gpu.Program(c["source"], c["dim"], list(params))
+        f = prog.integrand(params, low=[fx(x) for x in c["low"]], high=[fx(x) for x in c["high"]],
+                           n_samples=max(2, c["samples_per_cell"]), index=c["index"])
+        st, leaves = gpu.stratified_mc(f, c["cells_per_dim"], c["samples_per_cell"], c["seed"], c["trial"],
+                                       c["chunk_base"], c["cell_cap"])
+        want = c["estimate"]
+        assert st.status == want["status"], c["source"]
+        if want["status"] != gpu.TRIAL_OK:
+            assert leaves == []
+            continue
+        assert len(leaves) == want["n_leaves"] and st.n_samples == want["n_samples"]
+        for got, (lo, hi, val, se) in zip(leaves, c["leaves"]):
+            assert [got.low[j] for j in range(c["dim"])] == [fx(x) for x in lo]
+            assert [got.high[j] for j in range(c["dim"])] == [fx(x) for x in hi]
+            assert abs(got.estimate.value - fx(val)) <= 1e-12 * abs(fx(val)) + 1e-9 * fx(se), c["source"]
+        assert abs(st.value - fx(want["value"])) <= 1e-12 * abs(fx(want["value"])) + 1e-9 * fx(want["std_error"])
+        assert abs(st.std_error - fx(want["std_error"])) <= 1e-9 * fx(want["std_error"])
+    # the constant integrand: exactly the reference's value, zero error
+    const = [c for c in cases if c["source"] == "5"][0]
+    p5 = gpu.Program("5", 3)
+    st, _ = gpu.stratified_mc(p5.integrand(low=[0, 0, 0], high=[2, 1, 1], n_samples=100), 4, 100, 1)
+    assert st.value == fx(const["estimate"]["value"]) and st.std_error == 0.0
