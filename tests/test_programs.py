@@ -286,3 +286,21 @@ def test_jit_code_compiles_for_every_golden_program(mcb, progs, tmp_path, monkey
         p = mcb.Program(src, dim, names)
         p.jit_build()
     assert len(list(tmp_path.iterdir())) >= len(srcs) - 2  # cubins cached (duplicates share)
+
+
+@pytest.mark.gpu
+def test_jit_same_code_different_dimension(gpu):
+    """One instruction list in two dimensions is two specialised kernels (the
+    sampler's D differs): both bit-identical to the interpreter."""
+    assert gpu.program_jit(1)
+    p1, p3 = gpu.Program("x1*x1", 1), gpu.Program("x1*x1", 3)
+    fns = [p1.integrand(low=[0.0], high=[2.0], n_samples=50_000, index=0),
+           p3.integrand(low=[0.0, 0.0, 0.0], high=[2.0, 1.0, 1.0], n_samples=50_000, index=0)]
+    a = [gpu.run_direct([f], 5, 2) for f in fns]
+    gpu.program_jit(0)
+    try:
+        b = [gpu.run_direct([f], 5, 2) for f in fns]
+    finally:
+        gpu.program_jit(1)
+    for x, y in zip(a, b):
+        assert x.tobytes() == y.tobytes()
