@@ -1277,10 +1277,17 @@ mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
     for (size_t i : trees)
       for (uint32_t t = 0; t < trials; ++t)
         tasks.push_back(mcb::tree::TreeTask{&fns[i], t, 0, out + i * trials + t, nullptr});
+    std::mutex err_mu;
+    std::string err;
     if ((st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
-           return run_cells(batches, seed, devs);
+           const mcb_status s = run_cells(batches, seed, devs);
+           if (s != MCB_OK) {  // the driver may call from its own threads: keep the message
+             std::lock_guard<std::mutex> lk(err_mu);
+             err = g_last_error;
+           }
+           return s;
          })) != MCB_OK)
-      return st;
+      return fail(st, err);
   }
   const auto t1 = std::chrono::steady_clock::now();
   if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();

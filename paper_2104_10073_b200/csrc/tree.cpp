@@ -374,11 +374,14 @@ Config config_of(const mcb_integrand& f) {
   return c;
 }
 
-mcb_status run_trees(std::vector<TreeTask>& tasks, const CellRunner& run) {
-  std::vector<Tree> trees(tasks.size());
-  Pool pool(host_threads(tasks.size()));
+namespace {
+
+// All rounds of one group of trees (tasks[0, n)).
+mcb_status run_group(TreeTask* tasks, size_t n, const CellRunner& run, unsigned threads) {
+  std::vector<Tree> trees(n);
+  Pool pool(threads);
   // First pass (src/estimator.cpp:215-263): grid size, then every grid cell.
-  pool.run(tasks.size(), [&](size_t i) {
+  pool.run(n, [&](size_t i) {
     Tree& t = trees[i];
     t.task = &tasks[i];
     t.cfg = config_of(*tasks[i].fn);
@@ -450,6 +453,34 @@ mcb_status run_trees(std::vector<TreeTask>& tasks, const CellRunner& run) {
     if ((st = run_round(trees, run, pool)) != MCB_OK) return st;
   }
   pool.run(trees.size(), [&](size_t i) { finish(trees[i]); });
+  return MCB_OK;
+}
+
+}  // namespace
+
+// Large batches run as a few groups of trees on their own host threads:
+// while one group's cells are on the GPU (the runner serialises device work
+// per device), the others do their host work (selection, splits, results),
+// so host and device time overlap.  Each tree is computed exactly as alone.
+#ifndef MCB_TREE_GROUPS
+#define MCB_TREE_GROUPS 4
+#endif
+constexpr size_t kTreeGroups = MCB_TREE_GROUPS;
+mcb_status run_trees(std::vector<TreeTask>& tasks, const CellRunner& run) {
+  const size_t n = tasks.size();
+  const unsigned threads = host_threads(n);
+  const size_t groups = std::min<size_t>(kTreeGroups, std::max<size_t>(1, n / 256));
+  if (groups == 1) return run_group(tasks.data(), n, run, threads);
+  std::vector<mcb_status> st(groups, MCB_OK);
+  std::vector<std::thread> pool;
+  for (size_t g = 0; g < groups; ++g) {
+    const size_t b = n * g / groups, e = n * (g + 1) / groups;
+    const unsigned t = std::max(1u, unsigned(threads / groups));
+    pool.emplace_back([&, g, b, e, t] { st[g] = run_group(tasks.data() + b, e - b, run, t); });
+  }
+  for (auto& th : pool) th.join();
+  for (mcb_status s : st)
+    if (s != MCB_OK) return s;
   return MCB_OK;
 }
 
