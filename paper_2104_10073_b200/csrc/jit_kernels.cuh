@@ -23,6 +23,9 @@
 #ifndef MCB_JIT_THREADS
 #define MCB_JIT_THREADS 128  // = kProgThreads
 #endif
+#ifndef MCB_JIT_WARP_MIN_BLOCKS
+#define MCB_JIT_WARP_MIN_BLOCKS 8  // small-cell kernels are latency-bound: occupancy pays
+#endif
 
 namespace mcb {
 namespace jit {
@@ -227,7 +230,7 @@ __device__ __forceinline__ void tile_warp(const FnDesc* __restrict__ fns, const 
       NAME##_m2(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) { \
     mcb::jit::tile_cta<PROG, D, 2>(f, t, t0, p);                                                       \
   }                                                                                                    \
-  extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS)                                        \
+  extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS, MCB_JIT_WARP_MIN_BLOCKS)                                      \
       NAME##_m3(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) { \
     mcb::jit::tile_warp<PROG, D>(f, t, t0, p);                                                         \
   }

@@ -37,7 +37,8 @@ def main():
     def stratified(fns_seed_trials):
         fns, seed, trials = fns_seed_trials
         for f in fns:
-            mcb.stratify(f)
+            if isinstance(f, mcb.Integrand):
+                mcb.stratify(f)
         return fns, seed, trials
 
     builders = {
@@ -45,6 +46,7 @@ def main():
         "c2_strat": lambda: stratified(w.c2()),
         "c3_strat": lambda: stratified(w.c3()),
         "c1_program": lambda: as_program(w.c1()),
+        "c2_program_strat": lambda: stratified(as_program(w.c2())),
         "c2_program": lambda: as_program(w.c2()),
         "c1": lambda: w.c1(),
         "c2": lambda: w.c2(),
