@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
     ap.add_argument("--c5-fns", type=int, default=10000)
     ap.add_argument("--c4-trials", type=int, default=10)
+    ap.add_argument("--reference-seconds", type=float, default=0.0,
+                    help="also time the reference's own run_batch (oracle/_ref, all host threads) on a "
+                         "deterministic prefix of each config sized to about this many seconds")
     args = ap.parse_args()
     import torch
 
@@ -84,8 +87,27 @@ def main():
                      "philox_blocks_per_s": info.philox_blocks / t,
                      "frac_of_philox_peak": info.philox_blocks / t / peak,
                      "ok_trials": ok}
+        if args.reference_seconds > 0 and not keep:
+            out[name]["reference_cpu"] = reference_rate(fns, seed, trials, args.reference_seconds)
+            out[name]["speedup_vs_reference"] = out[name]["samples_per_s"] / out[name]["reference_cpu"]["samples_per_s"]
         print(name, json.dumps(out[name]), flush=True)
     print(json.dumps(out))
+
+
+def reference_rate(fns, seed, trials, target_s):
+    """The reference's run_batch on the first integrands of the config: a
+    calibration run on one, then a prefix sized to ~target_s."""
+    import os
+
+    from tests import _oracle
+    if _oracle.load_ref() is None:
+        return None
+    _, _, _, _, secs = _oracle.ref_run_batch(fns[:1], seed, trials, workers=0)
+    n = int(max(1, min(len(fns), target_s / max(secs, 1e-3))))
+    out, _, _, _, secs = _oracle.ref_run_batch(fns[:n], seed, trials, workers=0)
+    samples = int(out["n_samples"].sum())
+    return {"integrands": n, "of": len(fns), "threads": os.cpu_count(), "seconds": secs,
+            "samples_per_s": samples / secs}
 
 
 if __name__ == "__main__":
