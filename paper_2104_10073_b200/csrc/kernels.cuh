@@ -198,9 +198,15 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
   const uint64_t group = tile0 + uint64_t(blockIdx.x) * kTileAlign;
   const uint32_t fi = __ldg(tile_fn + group);
   FnDesc f = fns[fi];
-  __shared__ TrigAB ab[TABLE ? 512 : 1];
-  if (TABLE) {
-    build_trig_table<UNIT_COEF>(ab, f.a, f.b);
+  // Unit coefficients: A_m, B_m do not depend on the integrand, read through
+  // L1 from global memory — no per-CTA table, no barrier.  Otherwise the
+  // CTA's (a, b) table is staged in shared memory as in K3.
+  constexpr bool STAGE = TABLE && !UNIT_COEF;
+  __shared__ TrigAB ab_smem[STAGE ? 512 : 1];
+  const TrigAB* ab = ab_smem;
+  if (TABLE && UNIT_COEF) ab = dev::g_trig_unit_ab;
+  if (STAGE) {
+    build_trig_table<UNIT_COEF>(ab_smem, f.a, f.b);
     __syncthreads();
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
