@@ -529,6 +529,8 @@ struct HostPlan {
   std::vector<GroupLaunch> groups;
   std::vector<uint32_t> code;  // PROGRAM family: all distinct programs' words
   std::vector<double> consts;  //   and constant pools
+  std::vector<double> bounds;        // STRATIFIED: grid boundaries of every integrand
+  std::vector<int64_t> bounds_off;   //   per descriptor: offset into `bounds` (-1: none)
   uint64_t n_tiles = 0, total_samples = 0, philox_blocks = 0;
 };
 
@@ -554,6 +556,7 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     return kx < ky;
   });
   hp.descs.resize(n_fns);
+  hp.bounds_off.assign(n_fns, -1);
   std::map<const mcb_program*, std::pair<uint32_t, uint32_t>> prog_at;  // code, const offsets
   uint64_t tile = 0;
   for (size_t r = 0; r < n_fns; ++r) {
@@ -586,6 +589,15 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     hp.groups.back().n_tiles += nt;
     hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
     tile += nt;
+    if (d.strat_k > 0) {  // grid_cell boundaries, ref src/estimator.cpp:124-143 arithmetic
+      hp.bounds_off[r] = int64_t(hp.bounds.size());
+      const uint32_t k = d.strat_k;
+      for (uint32_t j = 0; j < fns[i].dim; ++j) {
+        const double lo = fns[i].low[j], width = fns[i].high[j] - fns[i].low[j];
+        for (uint32_t dg = 0; dg <= k; ++dg)
+          hp.bounds.push_back(dg == 0 ? lo : (dg == k ? fns[i].high[j] : lo + width * (double(dg) / k)));
+      }
+    }
     hp.descs[r] = d;
     hp.total_samples += trial_samples(fns[i]) * trials;
     uint64_t pairs;
@@ -613,6 +625,8 @@ struct DevBuf {
   mcb_trial_stats* out = nullptr;
   uint32_t* code = nullptr;
   double* consts = nullptr;
+  double* bounds = nullptr;             // stratified grid boundaries
+  size_t cap_bounds = 0;
   double* rects = nullptr;              // tree rounds: cell rectangles
   mcb::CellEst* cell_est = nullptr;     //   and per-cell estimates
   size_t cap_fns = 0, cap_tiles = 0, cap_part = 0, cap_out = 0, cap_code = 0, cap_consts = 0;
@@ -646,6 +660,7 @@ struct DevBuf {
     if (out) cudaFree(out);
     if (code) cudaFree(code);
     if (consts) cudaFree(consts);
+    if (bounds) cudaFree(bounds);
     if (rects) cudaFree(rects);
     if (cell_est) cudaFree(cell_est);
     *this = DevBuf{};
@@ -671,6 +686,10 @@ mcb_status enqueue_run(const HostPlan& hp, DevBuf& buf, uint32_t trials, const F
   if (upload) {
     if ((e = cudaMemcpyAsync(buf.fns, staged, sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice, s)) != cudaSuccess)
       return cuda_fail(e, "cudaMemcpyAsync(descriptors)");
+    if (!hp.bounds.empty() &&
+        (e = cudaMemcpyAsync(buf.bounds, hp.bounds.data(), sizeof(double) * hp.bounds.size(),
+                             cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync(grid bounds)");
     if (!hp.code.empty() &&
         ((e = cudaMemcpyAsync(buf.code, hp.code.data(), sizeof(uint32_t) * hp.code.size(),
                               cudaMemcpyHostToDevice, s)) != cudaSuccess ||
@@ -761,7 +780,11 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
     return cuda_fail(e, "cudaMalloc");
   if ((e = grow_pinned(c.h_descs, c.h_descs_cap, n_fns)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
   if ((e = grow_pinned(c.h_out, c.h_out_cap, n_out)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  if ((e = DevBuf::grow(c.buf.bounds, c.buf.cap_bounds, hp.bounds.size())) != cudaSuccess)
+    return cuda_fail(e, "cudaMalloc");
   std::memcpy(c.h_descs, hp.descs.data(), sizeof(FnDesc) * n_fns);
+  for (size_t r = 0; r < n_fns; ++r)
+    if (hp.bounds_off[r] >= 0) c.h_descs[r].grid_bounds = c.buf.bounds + hp.bounds_off[r];
   if ((st = enqueue_run(hp, c.buf, trials, c.h_descs, true, c.stream)) != MCB_OK) return st;
   if ((e = cudaMemcpyAsync(c.h_out, c.buf.out, sizeof(mcb_trial_stats) * n_out, cudaMemcpyDeviceToHost,
                            c.stream)) != cudaSuccess)
@@ -949,6 +972,12 @@ mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t see
   DeviceGuard guard(device);
   cudaError_t e = plan->buf.reserve(n_fns, plan->hp.n_tiles, n_fns * trials, plan->hp.code.size(),
                                     plan->hp.consts.size());
+  if (e == cudaSuccess) e = DevBuf::grow(plan->buf.bounds, plan->buf.cap_bounds, plan->hp.bounds.size());
+  if (e == cudaSuccess && !plan->hp.bounds.empty())
+    e = cudaMemcpy(plan->buf.bounds, plan->hp.bounds.data(), sizeof(double) * plan->hp.bounds.size(),
+                   cudaMemcpyHostToDevice);
+  for (size_t r = 0; r < n_fns; ++r)
+    if (plan->hp.bounds_off[r] >= 0) plan->hp.descs[r].grid_bounds = plan->buf.bounds + plan->hp.bounds_off[r];
   if (e == cudaSuccess)
     e = cudaMemcpy(plan->buf.fns, plan->hp.descs.data(), sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !plan->hp.code.empty())

@@ -40,6 +40,11 @@ __device__ double cell_volume(const FnDesc& F, uint32_t cell) {
   for (int j = int(F.dim) - 1; j >= 0; --j) {
     const uint32_t digit = rem % k;
     rem /= k;
+    if (F.grid_bounds) {  // host-computed boundaries (same arithmetic)
+      const double* b = F.grid_bounds + uint32_t(j) * (k + 1) + digit;
+      w[j] = __dsub_rn(b[1], b[0]);
+      continue;
+    }
     const double lo = F.low[j], wd = F.width[j];
     const double cl = digit == 0 ? lo : __dadd_rn(lo, __dmul_rn(wd, __ddiv_rn(double(digit), double(k))));
     const double ch = digit + 1 == k ? F.high[j]
