@@ -257,11 +257,14 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
   }
   // two pairs per iteration (q, q + 32): independent Philox / trig chains
   // interleave, as K3's software pipeline does; sums keep ascending q order
+  // round-1 products advance by 64-bit adds (as K3): M0*(q+32)D = M0*qD + M0*32D
+  constexpr uint64_t kStep32 = uint64_t(dev::kM0) * uint64_t(32 * D);
   uint32_t q = lane + 32;
-  for (; q + 32 < pairs; q += 64) {
+  uint64_t pq = uint64_t(dev::kM0) * uint64_t(q * uint32_t(D));
+  for (; q + 32 < pairs; q += 64, pq += 2 * kStep32) {
     double x0, x1, y0, y1;
-    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(q * uint32_t(D)), x0, x1);
-    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t((q + 32) * uint32_t(D)), y0, y1);
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, pq, x0, x1);
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, pq + kStep32, y0, y1);
     const double a0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
     const double a1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
     const double b0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, y0);
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
   }
   if (q < pairs) {
     double x0, x1;
-    dev::gen_pair<FAM, D, false, SAFE>(f, P, uint64_t(dev::kM0) * uint64_t(q * uint32_t(D)), x0, x1);
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, pq, x0, x1);
     add(q, dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0), dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1));
   }
 #pragma unroll
