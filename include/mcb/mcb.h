@@ -289,11 +289,15 @@ MCB_API mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32
                           uint64_t chunk, uint64_t first_point, uint64_t count,
                           int device, double* out);
 /* Runtime specialisation of PROGRAM integrands: each program is compiled by
- * NVRTC into straight-line sm_100a code (bit-identical results to the
- * bytecode interpreter, which runs when this is off or NVRTC is missing).
- * mode 1 = on (default unless MCB_PROGRAM_JIT=0), 0 = off, < 0 = query;
- * returns whether it is active.  Compiled cubins are cached in memory per
- * device and on disk ($MCB_JIT_CACHE, default ~/.cache/mcb-jit; "0" = off). */
+ * NVRTC into straight-line sm_100a code, bit-identical in results to the
+ * bytecode interpreter.  mode 0 = off (interpreter), 1 = automatic (default:
+ * specialised when the program's cubin is cached in memory or on disk, when
+ * a plan (mcb_plan_create) will relaunch it, or when one launch is large
+ * enough to repay the ~1 s compile), 2 = always (compile before the first
+ * launch), < 0 = query; MCB_PROGRAM_JIT=0 / =always select 0 / 2.  Returns
+ * the active mode (0 without NVRTC).  Cubins are cached in memory and on
+ * disk ($MCB_JIT_CACHE, default ~/.cache/mcb-jit; "0" = off); warm the cache
+ * ahead of time with mcb_program_jit_build. */
 MCB_API int mcb_program_jit(int mode);
 /* Compile a program's specialised kernels without a device (warms the disk
  * cache ahead of time; MCB_ERR_INVALID_ARGUMENT with the NVRTC log if the

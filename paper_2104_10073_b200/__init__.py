@@ -441,10 +441,11 @@ def debug_eval(f: Integrand, seed: int, trial: int, chunk: int, first_point: int
     return out
 
 
-def program_jit(mode: int = -1) -> bool:
-    """Runtime specialisation of DSL programs (NVRTC): 1 on, 0 off (bytecode
-    interpreter), -1 query.  Returns whether it is active."""
-    return bool(lib.mcb_program_jit(mode))
+def program_jit(mode: int = -1) -> int:
+    """Runtime specialisation of DSL programs (NVRTC): 0 off (bytecode
+    interpreter), 1 automatic (default: cached / plan / large launches),
+    2 always, -1 query.  Returns the active mode (0 without NVRTC)."""
+    return int(lib.mcb_program_jit(mode))
 
 
 def program_jit_compiles() -> int:

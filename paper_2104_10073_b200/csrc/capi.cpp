@@ -669,19 +669,20 @@ struct DevBuf {
 
 // Enqueue: descriptor upload (from `staged`, pinned or not) + tile table +
 // fused kernels + ordered combine, all on `s`.
-// Runtime-specialised kernels of the plan's programs, compiled in parallel
-// before the first launch (jit.hpp).
-void prepare_programs(const HostPlan& hp) {
+// Runtime-specialised kernels of the plan's programs (jit.hpp): cache
+// look-ups, and with `compile` (plans, which are relaunched) parallel
+// compiles of the missing ones before the first launch.
+void prepare_programs(const HostPlan& hp, bool compile) {
   std::vector<const mcb::prog::Program*> progs;
   for (const auto& g : hp.groups)
     if (g.prog && std::find(progs.begin(), progs.end(), g.prog) == progs.end()) progs.push_back(g.prog);
-  mcb::jit::prepare(progs);
+  mcb::jit::prepare(progs, compile);
 }
 
 mcb_status enqueue_run(const HostPlan& hp, DevBuf& buf, uint32_t trials, const FnDesc* staged,
                        bool upload, cudaStream_t s) {
   cudaError_t e;
-  if (upload) prepare_programs(hp);
+  if (upload) prepare_programs(hp, false);
   const uint32_t n_fns = uint32_t(hp.descs.size());
   if (upload) {
     if ((e = cudaMemcpyAsync(buf.fns, staged, sizeof(FnDesc) * n_fns, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -986,7 +987,7 @@ mcb_status plan_create_impl(const mcb_integrand* fns, size_t n_fns, uint64_t see
   if (e == cudaSuccess && !plan->hp.consts.empty())
     e = cudaMemcpy(plan->buf.consts, plan->hp.consts.data(), sizeof(double) * plan->hp.consts.size(),
                    cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) prepare_programs(plan->hp);
+  if (e == cudaSuccess) prepare_programs(plan->hp, true);
   if (e == cudaSuccess)
     e = mcb::detail::launch_expand_tiles(plan->buf.fns, uint32_t(n_fns), trials, plan->buf.tile_fn, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -1509,8 +1510,8 @@ mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial
 }
 
 int mcb_program_jit(int mode) {
-  if (mode >= 0) mcb::jit::set_enabled(mode != 0);
-  return mcb::jit::enabled() ? 1 : 0;
+  if (mode >= 0) mcb::jit::set_mode(mode);
+  return mcb::jit::mode();
 }
 
 uint64_t mcb_program_jit_compiles(void) { return mcb::jit::compile_count(); }

@@ -27,25 +27,33 @@ struct TilePartial;
 }
 namespace jit {
 
-// Process-wide switch: MCB_PROGRAM_JIT=0 in the environment disables it;
-// set_enabled() overrides.  enabled() is false when NVRTC is unavailable.
+// Process-wide mode: 0 off (bytecode interpreter), 1 automatic (default:
+// specialised kernels for programs whose cubin is cached — in memory or on
+// disk — or that a plan will reuse, or whose launch is large enough to repay
+// the ~1 s compile; the interpreter otherwise), 2 always (compile before the
+// first launch).  MCB_PROGRAM_JIT=0 / =always select 0 / 2; set_mode()
+// overrides.  enabled() / mode() report 0 when NVRTC is unavailable.  No
+// background threads: every compile completes inside the call that needs it.
 bool enabled();
+int mode();
+void set_mode(int m);
 void set_enabled(bool on);
 // Why the last compile or the NVRTC load failed ("" if none).
 std::string last_error();
 
-// Launch the specialised kernel of `p` in `mode` (0 direct, 1 direct on the
-// unit cube, 2 cells CTA-per-tile, 3 small cells warp-per-tile) over `ctas`
-// CTAs of 128 threads starting at tile `tile0`.  Returns false (nothing
-// launched) when JIT is off or the program could not be compiled, so the
-// caller runs the interpreter.
-bool launch(const prog::Program& p, int mode, uint32_t ctas, const dev::FnDesc* fns, const uint32_t* tile_fn,
-            uint64_t tile0, dev::TilePartial* part, cudaStream_t s, cudaError_t* err);
+// Launch the specialised kernel of `p` in kernel mode `mode` (0 direct, 1
+// direct on the unit cube, 2 cells CTA-per-tile, 3 small cells
+// warp-per-tile) over `ctas` CTAs of 128 threads starting at tile `tile0`;
+// `samples` (the launch's work) decides whether the automatic mode compiles
+// an uncached program.  Returns false (nothing launched) when the caller
+// should run the interpreter.
+bool launch(const prog::Program& p, int mode, uint32_t ctas, uint64_t samples, const dev::FnDesc* fns,
+            const uint32_t* tile_fn, uint64_t tile0, dev::TilePartial* part, cudaStream_t s, cudaError_t* err);
 
-// Compile (in parallel) and load the specialised modules of `programs` that
-// the current device does not have yet; launch() would otherwise compile
-// them one by one on first use.
-void prepare(const std::vector<const prog::Program*>& programs);
+// Ahead of launches: look the programs up in the disk cache and, with
+// `compile` (a plan that will be relaunched) or in mode 2, compile the
+// missing ones in parallel.
+void prepare(const std::vector<const prog::Program*>& programs, bool compile);
 
 // NVRTC-compile `p` (or find it in the disk cache) without a device: warms
 // the on-disk cache ahead of time and checks the generated code.

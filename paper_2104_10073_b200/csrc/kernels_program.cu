@@ -420,7 +420,9 @@ cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const 
   if (g.prog && n_ctas <= kMaxGrid) {  // runtime-specialised kernel of this program (jit.hpp)
     const int mode = (g.variant & kWarpTile) ? 3 : (g.variant & kStrat) ? 2 : (g.variant & kUnitDomain) ? 1 : 0;
     cudaError_t err = cudaSuccess;
-    if (jit::launch(*g.prog, mode, uint32_t(n_ctas), fns, tile_fn, g.tile0, part, s, &err)) return err;
+    if (jit::launch(*g.prog, mode, uint32_t(n_ctas), g.n_tiles * MCB_CHUNK_SIZE, fns, tile_fn, g.tile0, part, s,
+                    &err))
+      return err;
   }
   if (cudaError_t err = ensure_smem_optin(); err != cudaSuccess) return err;
   const size_t smem = program_smem_bytes(g.slots, g.dim);

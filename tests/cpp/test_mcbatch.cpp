@@ -5,6 +5,7 @@
 // Built and run by tests/test_cpp_api.py (pytest -m gpu).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numbers>
 #include <string>
@@ -435,19 +436,28 @@ static void stratified_cases() {
   CHECK_THROWS_AS(stratified_mc(f, 10, 10, StreamKey{3, 0, 0, 0}, 50), CellBudgetExceeded);
 }
 
+#define RUN(f)                                         \
+  do {                                                 \
+    if (std::getenv("MCB_TEST_TRACE")) {               \
+      std::fprintf(stderr, "[test] %s\n", #f);        \
+      std::fflush(stderr);                             \
+    }                                                  \
+    f();                                               \
+  } while (0)
+
 int main() {
-  constants_are_exact();
-  tree_cases();
-  stratified_cases();
-  mixed_dimension_batch();
-  validate_reports_every_violation();
-  device_invariance();
-  failing_integrand_isolated();
-  depends_only_on_seed_index_spec();
-  parameter_scans();
-  estimator_cases();
-  sampling_and_generator();
-  fig1_band();
+  RUN(constants_are_exact);
+  RUN(tree_cases);
+  RUN(stratified_cases);
+  RUN(mixed_dimension_batch);
+  RUN(validate_reports_every_violation);
+  RUN(device_invariance);
+  RUN(failing_integrand_isolated);
+  RUN(depends_only_on_seed_index_spec);
+  RUN(parameter_scans);
+  RUN(estimator_cases);
+  RUN(sampling_and_generator);
+  RUN(fig1_band);
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

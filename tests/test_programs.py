@@ -248,7 +248,7 @@ def test_jit_bit_identical_to_interpreter(gpu, progs):
     interpreter: every per-trial McEstimate byte-identical, in all four modes
     (direct, unit cube, cells CTA-per-tile, small cells warp-per-tile), for
     the golden programs incl. non-finite patterns and the random ones."""
-    assert gpu.program_jit(1), gpu.program_jit_error()
+    assert gpu.program_jit(2) == 2, gpu.program_jit_error()  # always: every launch specialised
     keep, fns = [], []
     for i, c in enumerate(progs):
         params, lo, hi = _case(c)
@@ -292,7 +292,7 @@ def test_jit_code_compiles_for_every_golden_program(mcb, progs, tmp_path, monkey
 def test_jit_same_code_different_dimension(gpu):
     """One instruction list in two dimensions is two specialised kernels (the
     sampler's D differs): both bit-identical to the interpreter."""
-    assert gpu.program_jit(1)
+    assert gpu.program_jit(2) == 2
     p1, p3 = gpu.Program("x1*x1", 1), gpu.Program("x1*x1", 3)
     fns = [p1.integrand(low=[0.0], high=[2.0], n_samples=50_000, index=0),
            p3.integrand(low=[0.0, 0.0, 0.0], high=[2.0, 1.0, 1.0], n_samples=50_000, index=0)]
@@ -304,3 +304,25 @@ def test_jit_same_code_different_dimension(gpu):
         gpu.program_jit(1)
     for x, y in zip(a, b):
         assert x.tobytes() == y.tobytes()
+
+
+@pytest.mark.gpu
+def test_jit_automatic_mode(gpu, tmp_path, monkeypatch):
+    """Default mode: a small one-shot run of an uncached program interprets
+    (no compile); after mcb_program_jit_build (or a plan) the cached cubin is
+    used — same bytes either way."""
+    monkeypatch.setenv("MCB_JIT_CACHE", str(tmp_path))  # a cold disk cache
+    assert gpu.program_jit(1) == 1
+    p = gpu.Program("exp(-b*(x1-0.25)^2) * (1 + 0.5*sin(9*x2)) + x1", 2, ["b"])
+    f = p.integrand({"b": 7.5}, n_samples=300_000, index=4)
+    n0 = gpu.program_jit_compiles()
+    first = gpu.run_direct([f], 17, 3)  # interpreter: not cached, too small to compile
+    assert gpu.program_jit_compiles() == n0
+    p.jit_build()
+    assert gpu.program_jit_compiles() == n0 + 1
+    later = gpu.run_direct([f], 17, 3)  # specialised (in memory now)
+    assert first.tobytes() == later.tobytes()
+    q = gpu.Program("exp(-b*(x1-0.25)^2) * (1 + 0.5*sin(9*x2)) + x2", 2, ["b"])
+    plan = gpu.Plan([q.integrand({"b": 7.5}, n_samples=300_000, index=4)], 17, 3)  # plans compile
+    assert gpu.program_jit_compiles() == n0 + 2
+    plan.close()

@@ -32,6 +32,7 @@ def main():
 
     import paper_2104_10073_b200 as mcb
     from paper_2104_10073_b200 import workloads as w
+    mcb.program_jit(2)  # DSL programs: specialised kernels from the first round on
 
     keep, sources = None, None
     if args.integrand == "peak":
