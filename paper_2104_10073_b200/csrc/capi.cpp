@@ -34,6 +34,7 @@
 #include "jit.hpp"
 #include "program.hpp"
 #include "tree.hpp"
+#include "tree_device.cuh"
 
 // Opaque compiled program of the C-ABI.
 struct mcb_program {
@@ -728,6 +729,16 @@ struct DeviceCtx {
   size_t h_rects_cap = 0;
   mcb::CellEst* h_cell_est = nullptr;
   size_t h_cell_est_cap = 0;
+  // device-resident tree runs
+  mcb::tdev::TreeConst* t_const = nullptr;
+  mcb::tdev::TreeState* t_state = nullptr;
+  uint64_t* t_groups = nullptr;
+  size_t cap_trees = 0, cap_tstate = 0, cap_tgroups = 0;
+  double *l_rect = nullptr, *l_new_rect = nullptr, *l_se = nullptr, *l_val = nullptr;
+  uint32_t *l_nn = nullptr, *l_depth = nullptr, *l_dead = nullptr, *l_new_leaf = nullptr;
+  mcb::CellEst* l_est = nullptr;
+  size_t cap_rect = 0, cap_new_rect = 0, cap_se = 0, cap_val = 0, cap_nn = 0, cap_depth = 0, cap_dead = 0,
+         cap_new_leaf = 0, cap_est = 0;
 };
 
 DeviceCtx& device_ctx(int device) {
@@ -935,6 +946,291 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
   return MCB_OK;
 }
 
+// Device-resident tree_refine for `tasks` on one device (tree_device.cuh):
+// the host builds each tree's first-pass grid and constants once; every
+// round then runs on the GPU with one small read-back (the launch groups'
+// tile ranges).  Results are those of the host driver (tree.cpp).
+mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t seed, int device) {
+  using namespace mcb::detail;
+  using mcb::tdev::TreeConst;
+  using mcb::tdev::TreeState;
+  const size_t T = tasks.size();
+  if (T == 0) return MCB_OK;
+  // ---- host: configs, first-pass grids, descriptors, launch groups ----
+  struct HostTree {
+    mcb::tree::Config cfg;
+    uint32_t k = 0, spc = 0, cpc = 0, fail = 0;
+    uint64_t n0 = 0, cap = 0;
+    Prepared prep;
+  };
+  std::vector<HostTree> ht(T);
+  for (size_t i = 0; i < T; ++i) {
+    const mcb_integrand& f = *tasks[i]->fn;
+    HostTree& h = ht[i];
+    h.cfg = mcb::tree::config_of(f);
+    h.spc = std::max<uint32_t>(h.cfg.samples_per_cell, 2);
+    h.cpc = uint32_t(chunk_count(h.spc));
+    uint32_t k = h.cfg.init_cells_per_dim;
+    bool ok = true;
+    if (k == 0) {  // src/estimator.cpp:219-228
+      k = auto_cells_per_dim(f.dim, 4096);
+      while (k > 1) {
+        uint64_t cells;
+        if (!cell_grid_size(k, f.dim, h.cfg.cell_cap, cells)) {
+          ok = false;
+          break;
+        }
+        if (cells * h.spc <= h.cfg.total_budget / 2) break;
+        --k;
+      }
+    }
+    if (!ok || !cell_grid_size(k, f.dim, h.cfg.cell_cap, h.n0)) {
+      h.fail = MCB_TRIAL_CELL_BUDGET;
+      h.n0 = 0;
+    } else if (tasks[i]->chunk_base + h.n0 * h.cpc - 1 > 0xFFFFFFFFull) {
+      h.fail = MCB_TRIAL_CHUNK_RANGE;
+      h.n0 = 0;
+    }
+    h.k = k;
+    const uint64_t first = h.n0 * h.spc;
+    const uint64_t splits = h.cfg.total_budget >= first ? (h.cfg.total_budget - first) / (2ull * h.spc) : 0;
+    h.cap = h.n0 + splits + 1;
+    if (h.cap > 0xFFFFFFFFull) return fail(MCB_ERR_INVALID_ARGUMENT, "tree budget too large for one device run");
+    h.prep = prepare(f, seed, 0, tasks[i]->trial, true);
+    if (h.spc <= kWarpTileMaxSpc) h.prep.variant |= kWarpTile;
+  }
+  std::vector<size_t> order(T);  // launch groups: (family, dim, variant, program)
+  std::iota(order.begin(), order.end(), size_t(0));
+  auto key = [&](size_t i) {
+    const mcb_integrand& f = *tasks[i]->fn;
+    return std::make_tuple(f.family, f.dim, ht[i].prep.variant,
+                           f.family == MCB_FAMILY_PROGRAM ? reinterpret_cast<uintptr_t>(f.program) : uintptr_t(0));
+  };
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return key(a) < key(b); });
+  HostPlan hp;
+  std::vector<TreeConst> tc(T);
+  std::vector<TreeState> tst(T);
+  std::map<const mcb_program*, std::pair<uint32_t, uint32_t>> prog_at;
+  uint64_t leaves = 0, rect_doubles = 0, max_tiles = 0;
+  hp.descs.resize(T);
+  for (size_t r = 0; r < T; ++r) {
+    const size_t i = order[r];
+    const mcb_integrand& f = *tasks[i]->fn;
+    HostTree& h = ht[i];
+    const int fam = int(f.family), dim = int(f.dim), var = h.prep.variant;
+    const mcb::prog::Program* gp = fam == MCB_FAMILY_PROGRAM ? &f.program->p : nullptr;
+    if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
+        hp.groups.back().variant != var || hp.groups.back().prog != gp)
+      hp.groups.push_back(GroupLaunch{fam, dim, var, 0, 0, 0, gp});
+    FnDesc d = h.prep.d;
+    d.strat_k = 0;
+    d.spc = h.spc;
+    d.cpc = h.cpc;
+    d.out_slot = r;
+    if (fam == MCB_FAMILY_PROGRAM) {
+      auto it = prog_at.find(f.program);
+      if (it == prog_at.end()) {
+        it = prog_at.emplace(f.program, std::make_pair(uint32_t(hp.code.size()), uint32_t(hp.consts.size()))).first;
+        hp.code.insert(hp.code.end(), f.program->words.begin(), f.program->words.end());
+        hp.consts.insert(hp.consts.end(), f.program->p.consts.begin(), f.program->p.consts.end());
+      }
+      d.prog_off = it->second.first;
+      d.prog_len = uint32_t(f.program->p.code.size());
+      d.const_off = it->second.second;
+      d.n_consts = uint32_t(f.program->p.consts.size());
+      hp.groups.back().slots = std::max(hp.groups.back().slots, f.program->p.depth);
+    }
+    hp.descs[r] = d;
+    TreeConst& c = tc[r];
+    c.leaf_off = leaves;
+    c.rect_off = rect_doubles;
+    c.budget = h.cfg.total_budget;
+    c.sigma = h.cfg.sigma_multiplier;
+    c.leaf_cap = uint32_t(h.cap);
+    c.dim = f.dim;
+    c.spc = h.spc;
+    c.cpc = h.cpc;
+    c.max_depth = h.cfg.max_depth;
+    c.warp_tiles = (var & kWarpTile) ? 1u : 0u;
+    c.group = uint32_t(hp.groups.size() - 1);
+    c.reserved = 0;
+    TreeState& st = tst[r];
+    std::memset(&st, 0, sizeof st);
+    st.fail = h.fail;
+    st.n_leaves = uint32_t(h.n0);
+    st.n_new = uint32_t(h.n0);
+    st.active = h.fail ? 0u : 1u;
+    st.chunk0 = tasks[i]->chunk_base;
+    st.next_chunk = tasks[i]->chunk_base + h.n0 * h.cpc;
+    st.used = h.n0 * h.spc;
+    leaves += h.cap;
+    rect_doubles += h.cap * 2 * f.dim;
+    max_tiles += (h.cap * h.cpc + kTileAlign - 1) / kTileAlign * kTileAlign;
+  }
+  max_tiles += kTileAlign * hp.groups.size();
+  if (hp.groups.size() > 256) return fail(MCB_ERR_INVALID_ARGUMENT, "too many distinct tree kernels in one run");
+  for (const auto& g : hp.groups)
+    if (g.family != MCB_FAMILY_PROGRAM && !variant_supported(g.family, g.dim, g.variant))
+      return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
+  // first-pass grids (grid_cell, src/estimator.cpp:124-143) = the initial
+  // leaves and round-0 cells, packed tree after tree (k_tree_init spreads them)
+  uint64_t packed_doubles = 0;
+  for (size_t r = 0; r < T; ++r) {
+    tc[r].init_off = packed_doubles;
+    packed_doubles += uint64_t(tst[r].n_leaves) * 2 * tc[r].dim;
+  }
+  DeviceCtx& c = device_ctx(device);
+  std::lock_guard<std::mutex> lock(c.mu);
+  DeviceGuard guard(device);
+  cudaError_t e;
+  if ((e = grow_pinned(c.h_rects, c.h_rects_cap, packed_doubles)) != cudaSuccess)
+    return cuda_fail(e, "cudaMallocHost");
+  for (size_t r = 0; r < T; ++r) {
+    const size_t i = order[r];
+    const mcb_integrand& f = *tasks[i]->fn;
+    const uint32_t k = ht[i].k, D = f.dim;
+    for (uint64_t cell = 0; cell < ht[i].n0; ++cell) {
+      double* lo = c.h_rects + tc[r].init_off + 2 * D * cell;
+      double* hi = lo + D;
+      uint64_t rem = cell;
+      for (uint32_t j = D; j-- > 0;) {
+        const uint32_t digit = uint32_t(rem % k);
+        rem /= k;
+        const double width = f.high[j] - f.low[j];
+        lo[j] = digit == 0 ? f.low[j] : f.low[j] + width * (double(digit) / k);
+        hi[j] = digit + 1 == k ? f.high[j] : f.low[j] + width * (double(digit + 1) / k);
+      }
+    }
+  }
+  // ---- device ----
+  if (!c.ready) {
+    if ((e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+    c.ready = true;
+  }
+  const cudaStream_t s = c.stream;
+  if ((e = c.buf.reserve(T, max_tiles, T, hp.code.size(), hp.consts.size())) != cudaSuccess ||
+      (e = DevBuf::grow(c.t_const, c.cap_trees, T)) != cudaSuccess ||
+      (e = DevBuf::grow(c.t_state, c.cap_tstate, T)) != cudaSuccess)
+    return cuda_fail(e, "cudaMalloc");
+  if ((e = DevBuf::grow(c.t_groups, c.cap_tgroups, 2 * hp.groups.size())) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_rect, c.cap_rect, rect_doubles)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_new_rect, c.cap_new_rect, rect_doubles)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_se, c.cap_se, leaves)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_val, c.cap_val, leaves)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_nn, c.cap_nn, leaves)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_depth, c.cap_depth, leaves)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_dead, c.cap_dead, leaves)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_new_leaf, c.cap_new_leaf, leaves)) != cudaSuccess ||
+      (e = DevBuf::grow(c.l_est, c.cap_est, leaves)) != cudaSuccess)
+    return cuda_fail(e, "cudaMalloc");
+  mcb::tdev::Leaves L{c.l_rect, c.l_se, c.l_val, c.l_nn, c.l_depth, c.l_dead, c.l_new_leaf, c.l_new_rect, c.l_est};
+  auto up = [&](void* dst, const void* src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+  };
+  if ((e = up(c.t_const, tc.data(), sizeof(TreeConst) * T)) != cudaSuccess ||
+      (e = up(c.t_state, tst.data(), sizeof(TreeState) * T)) != cudaSuccess ||
+      (e = up(c.buf.fns, hp.descs.data(), sizeof(FnDesc) * T)) != cudaSuccess ||
+      (e = DevBuf::grow(c.buf.rects, c.buf.cap_rects, packed_doubles)) != cudaSuccess ||
+      (e = up(c.buf.rects, c.h_rects, sizeof(double) * packed_doubles)) != cudaSuccess ||
+      (e = launch_tree_init(c.t_const, c.t_state, L, c.buf.rects, uint32_t(T), s)) != cudaSuccess ||
+      (!hp.code.empty() && (e = up(c.buf.code, hp.code.data(), sizeof(uint32_t) * hp.code.size())) != cudaSuccess) ||
+      (!hp.consts.empty() && (e = up(c.buf.consts, hp.consts.data(), sizeof(double) * hp.consts.size())) != cudaSuccess))
+    return cuda_fail(e, "cudaMemcpyAsync(tree setup)");
+  prepare_programs(hp, false);
+  std::vector<uint64_t> gt(2 * hp.groups.size());
+  for (int round = 0;; ++round) {
+    if (round > 0 && (e = launch_tree_select(c.t_const, c.t_state, L, uint32_t(T), s)) != cudaSuccess)
+      return cuda_fail(e, "launch k_tree_select");
+    if ((e = launch_tree_layout(c.t_const, c.t_state, c.buf.fns, L, uint32_t(T), c.t_groups,
+                                uint32_t(hp.groups.size()), s)) != cudaSuccess)
+      return cuda_fail(e, "launch k_tree_layout");
+    if ((e = cudaMemcpyAsync(gt.data(), c.t_groups, sizeof(uint64_t) * gt.size(), cudaMemcpyDeviceToHost, s)) !=
+            cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+      return cuda_fail(e, "tree round read-back");
+    uint64_t tiles = 0;
+    for (size_t g = 0; g < hp.groups.size(); ++g) tiles += gt[2 * g + 1];
+    if (tiles == 0) break;
+    if ((e = launch_expand_tiles(c.buf.fns, uint32_t(T), 1, c.buf.tile_fn, s)) != cudaSuccess)
+      return cuda_fail(e, "launch k_expand_tiles");
+    for (size_t g = 0; g < hp.groups.size(); ++g) {
+      if (gt[2 * g + 1] == 0) continue;
+      GroupLaunch gl = hp.groups[g];
+      gl.tile0 = gt[2 * g];
+      gl.n_tiles = gt[2 * g + 1];
+      e = gl.family == MCB_FAMILY_PROGRAM
+              ? launch_program_group(gl, c.buf.fns, c.buf.tile_fn, c.buf.part, c.buf.code, c.buf.consts, s)
+              : launch_direct_group(gl, c.buf.fns, c.buf.tile_fn, c.buf.part, s);
+      if (e != cudaSuccess) return cuda_fail(e, "launch tree cells");
+    }
+    if ((e = launch_combine(c.buf.fns, uint32_t(T), 1, c.buf.part, c.buf.out, s)) != cudaSuccess ||
+        (e = launch_tree_scatter(c.t_const, c.t_state, L, uint32_t(T), s)) != cudaSuccess)
+      return cuda_fail(e, "launch tree combine/scatter");
+  }
+  if ((e = launch_tree_finish(c.t_const, c.t_state, L, uint32_t(T), c.buf.out, s)) != cudaSuccess)
+    return cuda_fail(e, "launch k_tree_finish");
+  std::vector<mcb_trial_stats> out(T);
+  if ((e = cudaMemcpyAsync(out.data(), c.buf.out, sizeof(mcb_trial_stats) * T, cudaMemcpyDeviceToHost, s)) !=
+      cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync(tree results)");
+  bool want_leaves = false;
+  for (auto* t : tasks) want_leaves = want_leaves || t->leaves;
+  std::vector<double> h_rect, h_se, h_val;
+  std::vector<uint32_t> h_nn, h_depth, h_dead;
+  if (want_leaves) {
+    h_rect.resize(rect_doubles);
+    h_se.resize(leaves);
+    h_val.resize(leaves);
+    h_nn.resize(leaves);
+    h_depth.resize(leaves);
+    h_dead.resize(leaves);
+    if ((e = cudaMemcpyAsync(h_rect.data(), c.l_rect, sizeof(double) * rect_doubles, cudaMemcpyDeviceToHost, s)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(h_se.data(), c.l_se, sizeof(double) * leaves, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h_val.data(), c.l_val, sizeof(double) * leaves, cudaMemcpyDeviceToHost, s)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(h_nn.data(), c.l_nn, sizeof(uint32_t) * leaves, cudaMemcpyDeviceToHost, s)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(h_depth.data(), c.l_depth, sizeof(uint32_t) * leaves, cudaMemcpyDeviceToHost, s)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(h_dead.data(), c.l_dead, sizeof(uint32_t) * leaves, cudaMemcpyDeviceToHost, s)) !=
+            cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync(leaves)");
+  }
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  for (size_t r = 0; r < T; ++r) {
+    mcb::tree::TreeTask& task = *tasks[order[r]];
+    *task.out = out[r];
+    if (!task.leaves) continue;
+    task.leaves->clear();
+    if (out[r].status != MCB_TRIAL_OK) continue;  // leaves_out is written only when tree_refine returns
+    const uint32_t D = task.fn->dim, spc = tc[r].spc;
+    for (uint32_t i = 0; i < out[r].n_cells; ++i) {
+      const uint64_t l = tc[r].leaf_off + i;
+      mcb_leaf m;
+      std::memset(&m, 0, sizeof m);
+      std::memcpy(m.low, h_rect.data() + tc[r].rect_off + 2 * D * i, sizeof(double) * D);
+      std::memcpy(m.high, h_rect.data() + tc[r].rect_off + 2 * D * i + D, sizeof(double) * D);
+      m.depth = h_depth[l];
+      mcb_trial_stats& est = m.estimate;
+      est.n_samples = spc;
+      est.n_nonfinite = h_nn[l];
+      est.n_cells = 1;
+      if (h_dead[l]) {
+        est.status = MCB_TRIAL_ALL_NONFINITE;
+        est.nonfinite_warning = 1;
+      } else {
+        est.value = h_val[l];
+        est.std_error = h_se[l];
+        est.nonfinite_warning = double(h_nn[l]) > MCB_NONFINITE_WARN_FRACTION * double(spc) ? 1u : 0u;
+      }
+      task.leaves->push_back(m);
+    }
+  }
+  return MCB_OK;
+}
+
 }  // namespace
 
 struct mcb_plan {
@@ -1102,6 +1398,55 @@ mcb_status run_cells(const std::vector<mcb::tree::CellBatch>& batches, uint64_t 
   auto work = [&](size_t w) {
     if (shard[w].empty()) return;
     status[w] = run_cell_shard(shard[w], seed, devs[w]);
+    if (status[w] != MCB_OK) errors[w] = g_last_error;
+  };
+  if (devs.size() == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (size_t w = 0; w < devs.size(); ++w) pool.emplace_back(work, w);
+    for (auto& th : pool) th.join();
+  }
+  for (size_t w = 0; w < devs.size(); ++w)
+    if (status[w] != MCB_OK) return fail(status[w], "device " + std::to_string(devs[w]) + ": " + errors[w]);
+  return MCB_OK;
+}
+
+// Every tree of `tasks`, on `devs`: device-resident rounds (default; trees
+// sharded over the devices by budget, each device independent), or the host
+// driver over batched cell launches (MCB_TREE_DEVICE=0, kept as the
+// cross-check of the device rounds: both give identical trees).
+mcb_status run_trees_on(std::vector<mcb::tree::TreeTask>& tasks, uint64_t seed, const std::vector<int>& devs) {
+  static const bool host_driven = [] {
+    const char* e = std::getenv("MCB_TREE_DEVICE");
+    return e && e[0] == '0';
+  }();
+  if (host_driven) {
+    std::mutex err_mu;
+    std::string err;
+    const mcb_status st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
+      const mcb_status r = run_cells(batches, seed, devs);
+      if (r != MCB_OK) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        err = g_last_error;
+      }
+      return r;
+    });
+    return st == MCB_OK ? st : fail(st, err);
+  }
+  std::vector<std::vector<mcb::tree::TreeTask*>> shard(devs.size());
+  std::vector<double> load(devs.size(), 0.0);
+  for (auto& t : tasks) {  // greedy by budget (the trees' work bound)
+    size_t best = 0;
+    for (size_t w = 1; w < devs.size(); ++w)
+      if (load[w] < load[best]) best = w;
+    shard[best].push_back(&t);
+    load[best] += double(t.fn->n_samples) * sample_cost(*t.fn);
+  }
+  std::vector<mcb_status> status(devs.size(), MCB_OK);
+  std::vector<std::string> errors(devs.size());
+  auto work = [&](size_t w) {
+    status[w] = run_trees_device(shard[w], seed, devs[w]);
     if (status[w] != MCB_OK) errors[w] = g_last_error;
   };
   if (devs.size() == 1) {
@@ -1307,17 +1652,7 @@ mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
     for (size_t i : trees)
       for (uint32_t t = 0; t < trials; ++t)
         tasks.push_back(mcb::tree::TreeTask{&fns[i], t, 0, out + i * trials + t, nullptr});
-    std::mutex err_mu;
-    std::string err;
-    if ((st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
-           const mcb_status s = run_cells(batches, seed, devs);
-           if (s != MCB_OK) {  // the driver may call from its own threads: keep the message
-             std::lock_guard<std::mutex> lk(err_mu);
-             err = g_last_error;
-           }
-           return s;
-         })) != MCB_OK)
-      return fail(st, err);
+    if ((st = run_trees_on(tasks, seed, devs)) != MCB_OK) return st;
   }
   const auto t1 = std::chrono::steady_clock::now();
   if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
@@ -1339,9 +1674,7 @@ mcb_status mcb_tree_refine(const mcb_integrand* fn, uint64_t seed, uint32_t tria
   std::vector<mcb_leaf> lv;
   std::vector<mcb::tree::TreeTask> tasks{mcb::tree::TreeTask{&f, trial, chunk_base, out, &lv}};
   const std::vector<int> devs{device};
-  st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
-    return run_cells(batches, seed, devs);
-  });
+  st = run_trees_on(tasks, seed, devs);
   if (st != MCB_OK) return st;
   if (n_leaves) *n_leaves = lv.size();
   if (leaves)
@@ -1370,9 +1703,7 @@ mcb_status mcb_stratified_mc(const mcb_integrand* fn, uint32_t cells_per_dim, ui
   std::vector<mcb_leaf> lv;
   std::vector<mcb::tree::TreeTask> tasks{mcb::tree::TreeTask{&f, trial, chunk_base, out, &lv}};
   const std::vector<int> devs{device};
-  st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
-    return run_cells(batches, seed, devs);
-  });
+  st = run_trees_on(tasks, seed, devs);
   if (st != MCB_OK) return st;
   if (out->status == MCB_TRIAL_ALL_NONFINITE) {  // every cell dead: the first one throws
     out->status = MCB_TRIAL_DEAD_CELL;

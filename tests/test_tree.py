@@ -293,3 +293,42 @@ def test_tree_failure_statuses(gpu):
                           gpu.tree(gpu.harmonic(1.0, 2, n_samples=10_000, index=1), cell_cap=3)], 4, 2)
     assert list(out["status"][0]) == [gpu.TRIAL_OK] * 2
     assert list(out["status"][1]) == [gpu.TRIAL_CELL_BUDGET] * 2
+
+
+_CROSS = r"""
+import json, math, sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_2104_10073_b200 as mcb
+mcb.program_jit(0)
+peak = mcb.Program("exp(-100*((x1-c)^2+(x2-c)^2)) + sqrt(x1*x2)", 2, ["c"])
+fns = [mcb.tree(peak.integrand({{"c": 0.3 + 0.05 * i}}, n_samples=60_000, index=i), samples_per_cell=400)
+       for i in range(6)]
+fns += [mcb.tree(mcb.harmonic(20.0 + i, 3, a=0.5, b=1.5, n_samples=150_000, index=6 + i)) for i in range(4)]
+fns += [mcb.tree(mcb.make_integrand(mcb.FAMILY_ABS3, 3, a=1.2, n_samples=90_000, index=10), samples_per_cell=300,
+                 sigma_multiplier=0.2, max_depth=9)]
+out = mcb.run_direct(fns, 2468, 3)
+st, leaves = mcb.tree_refine(fns[0], 99, 1, 5, leaves=True)
+print(out.tobytes().hex())
+print(bytes(st).hex())
+print("".join(bytes(l).hex() for l in leaves))
+"""
+
+
+@pytest.mark.gpu
+def test_device_rounds_equal_host_driver(gpu, tmp_path):
+    """The device-resident rounds (default) and the host driver over batched
+    cell launches (MCB_TREE_DEVICE=0) build identical trees: every byte of
+    every result and leaf."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "cross.py"
+    script.write_text(_CROSS.format(root=root))
+    runs = []
+    for mode in ("1", "0"):
+        env = dict(os.environ, MCB_TREE_DEVICE=mode)
+        r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        runs.append(r.stdout)
+    assert runs[0] == runs[1]
