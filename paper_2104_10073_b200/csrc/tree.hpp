@@ -1,6 +1,8 @@
 // tree.hpp — host driver of the adaptive tree method,
 // tree_refine of ref src/estimator.cpp:184-318 run for many (integrand,
-// trial) trees at once.
+// trial) trees at once.  The default path keeps the leaves on the device
+// (tree_device.cuh); this host driver is the cross-check it is tested
+// against (MCB_TREE_DEVICE=0) and shares its configuration rules.
 //
 // tree_refine is sequential per tree (each round's split choice depends on
 // the previous round's cell estimates) but every cell estimate inside a round
