@@ -946,6 +946,32 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
   return MCB_OK;
 }
 
+// tree_refine's first-pass grid (src/estimator.cpp:219-231): cells per dim
+// and cell count; false = CellBudgetExceeded.
+bool tree_first_pass(const mcb_integrand& f, const mcb::tree::Config& cfg, uint32_t spc, uint32_t& k,
+                     uint64_t& n0) {
+  k = cfg.init_cells_per_dim;
+  if (k == 0) {
+    k = auto_cells_per_dim(f.dim, 4096);
+    while (k > 1) {
+      uint64_t cells;
+      if (!cell_grid_size(k, f.dim, cfg.cell_cap, cells)) return false;
+      if (cells * spc <= cfg.total_budget / 2) break;
+      --k;
+    }
+  }
+  return cell_grid_size(k, f.dim, cfg.cell_cap, n0);
+}
+
+// Most leaves a tree can reach: one per split the budget allows past the
+// first pass, and at most 2^max_depth per first-pass cell.
+uint64_t tree_leaf_bound(uint64_t n0, uint32_t spc, const mcb::tree::Config& cfg) {
+  const uint64_t first = n0 * spc;
+  const uint64_t splits = cfg.total_budget >= first ? (cfg.total_budget - first) / (2ull * spc) : 0;
+  const uint64_t by_depth = cfg.max_depth >= 40 ? ~0ull : n0 << cfg.max_depth;
+  return std::min(n0 + splits, std::max(n0, by_depth));
+}
+
 // Device-resident tree_refine for `tasks` on one device (tree_device.cuh):
 // the host builds each tree's first-pass grid and constants once; every
 // round then runs on the GPU with one small read-back (the launch groups'
@@ -970,21 +996,8 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     h.cfg = mcb::tree::config_of(f);
     h.spc = std::max<uint32_t>(h.cfg.samples_per_cell, 2);
     h.cpc = uint32_t(chunk_count(h.spc));
-    uint32_t k = h.cfg.init_cells_per_dim;
-    bool ok = true;
-    if (k == 0) {  // src/estimator.cpp:219-228
-      k = auto_cells_per_dim(f.dim, 4096);
-      while (k > 1) {
-        uint64_t cells;
-        if (!cell_grid_size(k, f.dim, h.cfg.cell_cap, cells)) {
-          ok = false;
-          break;
-        }
-        if (cells * h.spc <= h.cfg.total_budget / 2) break;
-        --k;
-      }
-    }
-    if (!ok || !cell_grid_size(k, f.dim, h.cfg.cell_cap, h.n0)) {
+    uint32_t k = 0;
+    if (!tree_first_pass(f, h.cfg, h.spc, k, h.n0)) {
       h.fail = MCB_TRIAL_CELL_BUDGET;
       h.n0 = 0;
     } else if (tasks[i]->chunk_base + h.n0 * h.cpc - 1 > 0xFFFFFFFFull) {
@@ -992,9 +1005,7 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
       h.n0 = 0;
     }
     h.k = k;
-    const uint64_t first = h.n0 * h.spc;
-    const uint64_t splits = h.cfg.total_budget >= first ? (h.cfg.total_budget - first) / (2ull * h.spc) : 0;
-    h.cap = h.n0 + splits + 1;
+    h.cap = tree_leaf_bound(h.n0, h.spc, h.cfg) + 1;
     if (h.cap > 0xFFFFFFFFull) return fail(MCB_ERR_INVALID_ARGUMENT, "tree budget too large for one device run");
     h.prep = prepare(f, seed, 0, tasks[i]->trial, true);
     if (h.spc <= kWarpTileMaxSpc) h.prep.variant |= kWarpTile;
@@ -1422,6 +1433,29 @@ mcb_status run_trees_on(std::vector<mcb::tree::TreeTask>& tasks, uint64_t seed, 
     return e && e[0] == '0';
   }();
   if (host_driven) {
+    std::mutex err_mu;
+    std::string err;
+    const mcb_status st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
+      const mcb_status r = run_cells(batches, seed, devs);
+      if (r != MCB_OK) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        err = g_last_error;
+      }
+      return r;
+    });
+    return st == MCB_OK ? st : fail(st, err);
+  }
+  // leaf storage is reserved up front on the device: very large trees (a
+  // budget / depth allowing > 64 Mi leaves in one call) take the host driver
+  uint64_t bound = 0;
+  for (auto& t : tasks) {
+    const mcb::tree::Config cfg = mcb::tree::config_of(*t.fn);
+    const uint32_t spc = std::max<uint32_t>(cfg.samples_per_cell, 2);
+    uint32_t k;
+    uint64_t n0;
+    if (tree_first_pass(*t.fn, cfg, spc, k, n0)) bound += tree_leaf_bound(n0, spc, cfg);
+  }
+  if (bound > (uint64_t(1) << 26)) {
     std::mutex err_mu;
     std::string err;
     const mcb_status st = mcb::tree::run_trees(tasks, [&](const std::vector<mcb::tree::CellBatch>& batches) {
