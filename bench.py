@@ -52,6 +52,9 @@ def parse():
                    help="target CPU seconds for the cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-clocks", action="store_true")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="weak: every rank integrates its own --n-fns set (default, the driver's scaling run); "
+                        "strong: the ranks split one --n-fns set")
     return p.parse_args()
 
 
@@ -89,6 +92,11 @@ class Dist:
     def close(self):
         if self.pg:
             self.pg.destroy_process_group()
+
+
+def strong_slice(n_fns: int, rank: int, world: int):
+    """Strong scaling: rank r integrates [lo, hi) of the one n_fns set."""
+    return n_fns * rank // world, n_fns * (rank + 1) // world
 
 
 def shard_first_index(rank: int, n_fns: int) -> int:
@@ -218,8 +226,13 @@ def run_mcb_arm(args, dist, local):
 
     torch.cuda.set_device(local)
     dev = local
-    first = shard_first_index(dist.rank, args.n_fns)
-    fns, seed, trials = workloads.c2(samples=args.samples, n_count=args.n_fns, first_index=first)
+    if args.scaling == "strong":  # one C2 set, rank r integrates its contiguous slice
+        fns, seed, trials = workloads.c2(samples=args.samples, n_count=args.n_fns)
+        lo, hi = strong_slice(args.n_fns, dist.rank, dist.world)
+        fns = fns[lo:hi]
+    else:
+        first = shard_first_index(dist.rank, args.n_fns)
+        fns, seed, trials = workloads.c2(samples=args.samples, n_count=args.n_fns, first_index=first)
     arr = mcb.as_array(fns)
     stream = torch.cuda.current_stream()
     plan = mcb.Plan(arr, seed, trials, device=dev)
@@ -265,7 +278,8 @@ def run_mcb_arm(args, dist, local):
     e2e_s = dist.max(sum(e2e_times), device=f"cuda:{dev}")
     assert out.tobytes() == res.tobytes(), "plan and C-ABI results differ"
 
-    total_samples = info.total_samples * dist.world * args.steps
+    job_samples = args.samples * trials * (args.n_fns if args.scaling == "strong" else args.n_fns * dist.world)
+    total_samples = job_samples * args.steps
     value = total_samples / kernel_s_max
     e2e_value = total_samples / e2e_s
 
@@ -282,12 +296,13 @@ def run_mcb_arm(args, dist, local):
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * kernel_s_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": CONFIG_NAME, "integrands_per_gpu": args.n_fns,
+        "config": {"workload": CONFIG_NAME,
+                   "integrands_per_gpu": args.n_fns if args.scaling == "weak" else len(fns),
                    "samples_per_integrand": args.samples, "trials": trials, "seed": seed,
                    "family": "cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4)), k_n=(n+50)/2pi, [0,1]^4",
-                   "parallelism": f"weak dp{dist.world} (integrand shards, no collective)",
+                   "parallelism": f"{args.scaling} dp{dist.world} (integrand shards, no collective)",
                    "l2": "flushed (256 MB write) between timed iterations; inputs are ~230 KB of descriptors",
                    "seconds_per_1000_fn_set": 1e-3 * (1e3 * kernel_s_max / args.steps) * 1000 / args.n_fns,
                    "tiles_per_step": info.n_tiles, "wall_s_timed_region": wall},

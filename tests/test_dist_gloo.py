@@ -96,3 +96,13 @@ def test_reference_arm_json_contract():
         assert k in line
     assert line["cpu_baseline"]["kind"] == ("reference" if os.path.exists(ref_so) else "port")
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
+
+
+def test_strong_scaling_slices_cover_the_set_once():
+    import bench
+    for world in (1, 2, 3, 4, 8):
+        seen = []
+        for rank in range(world):
+            lo, hi = bench.strong_slice(1000, rank, world)
+            seen.extend(range(lo, hi))
+        assert seen == list(range(1000))
