@@ -293,7 +293,7 @@ MCB_API mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32
  * bytecode interpreter.  mode 0 = off (interpreter), 1 = automatic (default:
  * specialised when the program's cubin is cached in memory or on disk, when
  * a plan (mcb_plan_create) will relaunch it, or when one launch is large
- * enough to repay the ~1 s compile), 2 = always (compile before the first
+ * enough to repay its ~0.3 s compile), 2 = always (compile before the first
  * launch), < 0 = query; MCB_PROGRAM_JIT=0 / =always select 0 / 2.  Returns
  * the active mode (0 without NVRTC).  Cubins are cached in memory and on
  * disk ($MCB_JIT_CACHE, default ~/.cache/mcb-jit; "0" = off); warm the cache

@@ -674,10 +674,17 @@ struct DevBuf {
 // look-ups, and with `compile` (plans, which are relaunched) parallel
 // compiles of the missing ones before the first launch.
 void prepare_programs(const HostPlan& hp, bool compile) {
-  std::vector<const mcb::prog::Program*> progs;
-  for (const auto& g : hp.groups)
-    if (g.prog && std::find(progs.begin(), progs.end(), g.prog) == progs.end()) progs.push_back(g.prog);
-  mcb::jit::prepare(progs, compile);
+  using mcb::detail::kStrat;
+  using mcb::detail::kUnitDomain;
+  using mcb::detail::kWarpTile;
+  std::vector<std::pair<const mcb::prog::Program*, int>> kernels;
+  for (const auto& g : hp.groups) {
+    if (!g.prog) continue;
+    const int km = (g.variant & kWarpTile) ? 3 : (g.variant & kStrat) ? 2 : (g.variant & kUnitDomain) ? 1 : 0;
+    const auto k = std::make_pair(g.prog, km);
+    if (std::find(kernels.begin(), kernels.end(), k) == kernels.end()) kernels.push_back(k);
+  }
+  mcb::jit::prepare(kernels, compile);
 }
 
 mcb_status enqueue_run(const HostPlan& hp, DevBuf& buf, uint32_t trials, const FnDesc* staged,

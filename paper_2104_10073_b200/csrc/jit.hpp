@@ -15,6 +15,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace mcb {
@@ -30,7 +31,7 @@ namespace jit {
 // Process-wide mode: 0 off (bytecode interpreter), 1 automatic (default:
 // specialised kernels for programs whose cubin is cached — in memory or on
 // disk — or that a plan will reuse, or whose launch is large enough to repay
-// the ~1 s compile; the interpreter otherwise), 2 always (compile before the
+// its ~0.3 s compile; the interpreter otherwise), 2 always (compile before the
 // first launch).  MCB_PROGRAM_JIT=0 / =always select 0 / 2; set_mode()
 // overrides.  enabled() / mode() report 0 when NVRTC is unavailable.  No
 // background threads: every compile completes inside the call that needs it.
@@ -50,13 +51,15 @@ std::string last_error();
 bool launch(const prog::Program& p, int mode, uint32_t ctas, uint64_t samples, const dev::FnDesc* fns,
             const uint32_t* tile_fn, uint64_t tile0, dev::TilePartial* part, cudaStream_t s, cudaError_t* err);
 
-// Ahead of launches: look the programs up in the disk cache and, with
+// Ahead of launches, for (program, kernel mode) pairs: look the kernels up in
+// the disk cache and, with
 // `compile` (a plan that will be relaunched) or in mode 2, compile the
 // missing ones in parallel.
-void prepare(const std::vector<const prog::Program*>& programs, bool compile);
+void prepare(const std::vector<std::pair<const prog::Program*, int>>& kernels, bool compile);
 
-// NVRTC-compile `p` (or find it in the disk cache) without a device: warms
-// the on-disk cache ahead of time and checks the generated code.
+// NVRTC-compile `p`'s four kernel modes (or find them in the disk cache)
+// without a device: warms the on-disk cache ahead of time and checks the
+// generated code.
 bool compile_only(const prog::Program& p, std::string* err);
 
 // Number of NVRTC compilations performed so far (tests / tracing).

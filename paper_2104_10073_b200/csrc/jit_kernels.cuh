@@ -216,21 +216,18 @@ __device__ __forceinline__ void tile_warp(const FnDesc* __restrict__ fns, const 
 }  // namespace jit
 }  // namespace mcb
 
-// One program's four entry points (extern "C" names: <name>_m<mode>).
-#define MCB_JIT_KERNELS(NAME, PROG, D)                                                                 \
-  extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS)                                        \
-      NAME##_m0(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) { \
-    mcb::jit::tile_cta<PROG, D, 0>(f, t, t0, p);                                                       \
-  }                                                                                                    \
-  extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS)                                        \
-      NAME##_m1(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) { \
-    mcb::jit::tile_cta<PROG, D, 1>(f, t, t0, p);                                                       \
-  }                                                                                                    \
-  extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS)                                        \
-      NAME##_m2(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) { \
-    mcb::jit::tile_cta<PROG, D, 2>(f, t, t0, p);                                                       \
-  }                                                                                                    \
-  extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS, MCB_JIT_WARP_MIN_BLOCKS)                                      \
-      NAME##_m3(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) { \
-    mcb::jit::tile_warp<PROG, D>(f, t, t0, p);                                                         \
+// One entry point `NAME` for kernel mode MODE (0 direct, 1 unit cube,
+// 2 cells CTA-per-tile, 3 small cells warp-per-tile): only the mode a
+// launch needs is compiled.
+template <int MODE>
+struct JitBounds {
+  static constexpr int min_blocks = MODE == 3 ? MCB_JIT_WARP_MIN_BLOCKS : 1;
+};
+#define MCB_JIT_KERNEL(NAME, PROG, D, MODE)                                                         \
+  extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS, JitBounds<MODE>::min_blocks)        \
+      NAME(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) {   \
+    if constexpr (MODE == 3)                                                                        \
+      mcb::jit::tile_warp<PROG, D>(f, t, t0, p);                                                    \
+    else                                                                                            \
+      mcb::jit::tile_cta<PROG, D, MODE>(f, t, t0, p);                                               \
   }

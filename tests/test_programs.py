@@ -279,13 +279,12 @@ def test_jit_code_compiles_for_every_golden_program(mcb, progs, tmp_path, monkey
     """The generated straight-line code of every golden program (and a few
     edge cases) compiles under NVRTC for sm_100a — no device needed."""
     monkeypatch.setenv("MCB_JIT_CACHE", str(tmp_path))
-    srcs = [(c["source"], c["dim"], list(c["params"])) for c in progs[:6]]
-    srcs += [("7", 1, []), ("x1", 1, []), ("-(-x2)", 2, []), ("1e308*1e308 - x1", 1, []),
-             ("sin(x1)*cos(x1) + sin(x1)", 1, []), ("a+b+c+d+e2+f+g+h", 1, list("abcdfgh") + ["e2"])]
+    srcs = [(c["source"], c["dim"], list(c["params"])) for c in progs[:3]]
+    srcs += [("7", 1, []), ("1e308*1e308 - x1", 1, []), ("a+b+c+d+e2+f+g+h", 1, list("abcdfgh") + ["e2"])]
     for src, dim, names in srcs:
         p = mcb.Program(src, dim, names)
         p.jit_build()
-    assert len(list(tmp_path.iterdir())) >= len(srcs) - 2  # cubins cached (duplicates share)
+    assert len(list(tmp_path.iterdir())) >= 4 * len(srcs)  # four kernel modes each, cached
 
 
 @pytest.mark.gpu
@@ -318,11 +317,11 @@ def test_jit_automatic_mode(gpu, tmp_path, monkeypatch):
     n0 = gpu.program_jit_compiles()
     first = gpu.run_direct([f], 17, 3)  # interpreter: not cached, too small to compile
     assert gpu.program_jit_compiles() == n0
-    p.jit_build()
-    assert gpu.program_jit_compiles() == n0 + 1
+    p.jit_build()  # all four kernel modes
+    assert gpu.program_jit_compiles() == n0 + 4
     later = gpu.run_direct([f], 17, 3)  # specialised (in memory now)
     assert first.tobytes() == later.tobytes()
     q = gpu.Program("exp(-b*(x1-0.25)^2) * (1 + 0.5*sin(9*x2)) + x2", 2, ["b"])
-    plan = gpu.Plan([q.integrand({"b": 7.5}, n_samples=300_000, index=4)], 17, 3)  # plans compile
-    assert gpu.program_jit_compiles() == n0 + 2
+    plan = gpu.Plan([q.integrand({"b": 7.5}, n_samples=300_000, index=4)], 17, 3)  # plans compile their mode
+    assert gpu.program_jit_compiles() == n0 + 5
     plan.close()
