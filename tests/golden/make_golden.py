@@ -168,6 +168,9 @@ def main():
     # 7. arbitrary DSL programs (the GPU interpreter's parity anchors)
     g["programs"] = make_program_goldens(ref)
 
+    # 7b. a wider random program sample: dims 1-6, random boxes, 4 parameters
+    g["programs_wide"] = make_wide_program_goldens(ref)
+
     # 8. tree method: tree_refine (src/estimator.cpp:212-318) standalone with
     # leaves, and run_batch's Tree branch (src/batch.cpp:276-289)
     g["tree"] = make_tree_goldens(ref)
@@ -345,6 +348,36 @@ def make_stratified_mc_goldens():
                     "cell_cap": cap, "estimate": dict(stats_json(st), n_leaves=len(leaves)),
                     "leaves": [[[H(l.low[j]) for j in range(dim)], [H(l.high[j]) for j in range(dim)],
                                 H(l.estimate.value), H(l.estimate.std_error)] for l in leaves]})
+    return out
+
+
+def make_wide_program_goldens(ref):
+    rng = np.random.default_rng(91)
+    out = []
+    for i in range(64):
+        dim = int(rng.integers(1, 7))
+        names = ["a", "b", "c", "d"][: int(rng.integers(0, 5))]
+        src = random_source(rng, dim, names, max_depth=int(rng.integers(2, 6)))
+        params = {n: float(np.round(rng.uniform(-3, 3), 6)) for n in names}
+        lo = np.round(rng.uniform(-2, 1, dim), 4)
+        hi = lo + np.round(rng.uniform(0.25, 3, dim), 4)
+        seed, index, trial, cb = int(rng.integers(0, 2**40)), i, int(rng.integers(0, 5)), int(rng.integers(0, 4))
+        n = int(rng.integers(2, 90_000))
+        nm = sorted(params)
+        cn = (ctypes.c_char_p * max(1, len(nm)))(*[x.encode() for x in nm])
+        vals = (ctypes.c_double * max(1, len(nm)))(*[params[x] for x in nm])
+        lo_c, hi_c = (ctypes.c_double * dim)(*lo), (ctypes.c_double * dim)(*hi)
+        pts = np.zeros(32 * dim)
+        assert ref.ref_sample_uniform(dim, lo_c, hi_c, seed, index, trial, cb, 32, pts.ctypes.data) == 0
+        v = np.zeros(32)
+        assert ref.ref_eval_source(src.encode(), dim, cn, vals, len(nm), pts.ctypes.data, 32, v.ctypes.data) == 0
+        st = mcb.TrialStats()
+        assert ref.ref_direct_mc_source(src.encode(), dim, cn, vals, len(nm), lo_c, hi_c, n, seed, index, trial, cb,
+                                        ctypes.byref(st)) == 0
+        out.append({"source": src, "dim": dim, "params": {k: H(x) for k, x in params.items()},
+                    "low": [H(float(x)) for x in lo], "high": [H(float(x)) for x in hi], "n_samples": n,
+                    "seed": seed, "index": index, "trial": trial, "chunk_base": cb,
+                    "values": [H(float(x)) for x in v], "estimate": stats_json(st)})
     return out
 
 

@@ -325,3 +325,38 @@ def test_jit_automatic_mode(gpu, tmp_path, monkeypatch):
     plan = gpu.Plan([q.integrand({"b": 7.5}, n_samples=300_000, index=4)], 17, 3)  # plans compile their mode
     assert gpu.program_jit_compiles() == n0 + 5
     plan.close()
+
+
+@pytest.mark.gpu
+def test_wide_random_programs_vs_reference_golden(gpu):
+    """64 more random programs (dims 1-6, random boxes, up to 4 parameters,
+    depth 2-5) against the reference's own values and estimates: per-sample
+    values through the interpreter, estimates through both the interpreter and
+    the specialised kernels."""
+    with open(GOLDEN) as fh:
+        cases = json.load(fh)["programs_wide"]
+    keep, fns = [], []
+    for c in cases:
+        params, lo, hi = _case(c)
+        p = gpu.Program(c["source"], c["dim"], list(params))
+        keep.append(p)
+        f = p.integrand(params, low=lo, high=hi, n_samples=c["n_samples"], index=c["index"])
+        got = gpu.debug_eval(f, c["seed"], c["trial"], c["chunk_base"], 0, 32)
+        want = np.array([fx(v) for v in c["values"]])
+        assert _values_close(got, want), c["source"]
+        fns.append((f, c))
+    for jit in (0, 2):
+        gpu.program_jit(jit)
+        try:
+            for f, c in fns:
+                st = gpu.direct_mc(f, c["seed"], c["trial"], c["chunk_base"])
+                e = c["estimate"]
+                assert st.status == e["status"], (jit, c["source"])
+                assert (st.n_samples, st.n_nonfinite) == (e["n_samples"], e["n_nonfinite"]), (jit, c["source"])
+                if e["status"] != 0:
+                    continue
+                want, se = fx(e["value"]), fx(e["std_error"])
+                assert abs(st.value - want) <= 1e-9 * abs(want) + 1e-7 * se + 1e-300, (jit, c["source"], st.value, want)
+                assert abs(st.std_error - se) <= 1e-9 * se + 1e-300, (jit, c["source"])
+        finally:
+            gpu.program_jit(1)
