@@ -1,18 +1,19 @@
-// capi.cpp — the C-ABI layer (include/mcb/mcb.h): validation, descriptor
-// lowering, device plans and the multi-GPU host scheduler.
+// capi.cpp — the C-ABI entry points (include/mcb/mcb.h), device plans and
+// the multi-GPU host scheduler; descriptor lowering and validation live in
+// capi_plan.cpp, the tree runners in capi_tree.cpp.
 //
 // Reference correspondence (file:line under /root/reference/proj):
 //   mcb_validate        validate                 src/batch.cpp:62-120
-//   mcb_run_direct      run_batch (Direct)       src/batch.cpp:195-333
+//   mcb_run_direct      run_batch                src/batch.cpp:195-333
 //   mcb_direct_mc       direct_mc                src/estimator.cpp:75-92
-//   mcb_tree_refine     tree_refine              src/estimator.cpp:212-318 (tree.cpp)
+//   mcb_tree_refine     tree_refine              src/estimator.cpp:212-318 (capi_tree.cpp)
 //   mcb_stratified_mc   stratified_mc            src/estimator.cpp:161-182
 //   mcb_summarize_trials summarize_trials        src/estimator.cpp:320-337
 //   mcb_stream_key      UniformStream key        src/sampling.cpp:84-87
 //   mcb_volume          HyperRect::volume        src/sampling.cpp:16-20
 //   mcb_debug_points    sample_uniform           src/sampling.cpp:102-112
 // There is no CPU fallback: every numeric result comes from the sm_100a
-// kernels in direct.cu; without a device the compute entry points return
+// kernels; without a device the compute entry points return
 // MCB_ERR_NO_DEVICE.
 #include <cuda_runtime.h>
 
