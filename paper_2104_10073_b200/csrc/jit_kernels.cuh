@@ -80,7 +80,19 @@ template <class P, int D, bool UNIT_DOM>
 __device__ __forceinline__ void accumulate(const FnDesc& f, const PhiloxPrefix& Ph, const double* params,
                                            uint32_t first, uint32_t stride, uint32_t pairs, uint32_t count,
                                            double& s1, double& s2, uint32_t& nbad) {
-  for (uint32_t q = first; q < pairs; q += stride) {
+  // two pairs per iteration: independent Philox / evaluation chains interleave
+  // (the sums still take the pairs in ascending order, as the interpreter)
+  uint32_t q = first;
+  for (; q + stride < pairs; q += 2 * stride) {
+    double x0[D], x1[D], y0[D], y1[D];
+    gen_points<D, UNIT_DOM>(f, Ph, q, x0, x1);
+    gen_points<D, UNIT_DOM>(f, Ph, q + stride, y0, y1);
+    const double a0 = P::eval(x0, params), a1 = P::eval(x1, params);
+    const double b0 = P::eval(y0, params), b1 = P::eval(y1, params);
+    add_pair(f, q, count, a0, a1, s1, s2, nbad);
+    add_pair(f, q + stride, count, b0, b1, s1, s2, nbad);
+  }
+  if (q < pairs) {
     double x0[D], x1[D];
     gen_points<D, UNIT_DOM>(f, Ph, q, x0, x1);
     add_pair(f, q, count, P::eval(x0, params), P::eval(x1, params), s1, s2, nbad);
