@@ -190,6 +190,12 @@ uint64_t tree_leaf_bound(uint64_t n0, uint32_t spc, const mcb::tree::Config& cfg
 // tile ranges).  Results are those of the host driver (tree.cpp).
 mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t seed, int device) {
   using namespace mcb::detail;
+  using tclk = std::chrono::steady_clock;
+  const auto t_start = tclk::now();
+  static const bool trace = [] {
+    const char* v = std::getenv("MCB_TREE_TRACE");
+    return v && *v && *v != '0';
+  }();
   using mcb::tdev::TreeConst;
   using mcb::tdev::TreeState;
   const size_t T = tasks.size();
@@ -202,9 +208,22 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     Prepared prep;
   };
   std::vector<HostTree> ht(T);
+  std::map<const mcb_integrand*, size_t> first_of;  // trials of one integrand share grid and descriptor
   for (size_t i = 0; i < T; ++i) {
     const mcb_integrand& f = *tasks[i]->fn;
     HostTree& h = ht[i];
+    auto seen = first_of.find(tasks[i]->fn);
+    if (seen != first_of.end()) {
+      h = ht[seen->second];
+      h.prep.d.trial_base = tasks[i]->trial;
+      if (!h.fail && tasks[i]->chunk_base + h.n0 * h.cpc - 1 > 0xFFFFFFFFull) {
+        h.fail = MCB_TRIAL_CHUNK_RANGE;
+        h.n0 = 0;
+        h.cap = tree_leaf_bound(0, h.spc, h.cfg) + 1;
+      }
+      continue;
+    }
+    first_of.emplace(tasks[i]->fn, i);
     h.cfg = mcb::tree::config_of(f);
     h.spc = std::max<uint32_t>(h.cfg.samples_per_cell, 2);
     h.cpc = uint32_t(chunk_count(h.spc));
@@ -308,10 +327,18 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
   cudaError_t e;
   if ((e = grow_pinned(c.h_rects, c.h_rects_cap, packed_doubles)) != cudaSuccess)
     return cuda_fail(e, "cudaMallocHost");
+  std::map<const mcb_integrand*, uint64_t> grid_at;  // packed offset of an integrand's grid
   for (size_t r = 0; r < T; ++r) {
     const size_t i = order[r];
     const mcb_integrand& f = *tasks[i]->fn;
     const uint32_t k = ht[i].k, D = f.dim;
+    if (ht[i].n0 == 0) continue;
+    auto done = grid_at.find(tasks[i]->fn);
+    if (done != grid_at.end()) {  // another trial of the same integrand: same grid
+      std::memcpy(c.h_rects + tc[r].init_off, c.h_rects + done->second, sizeof(double) * 2 * D * ht[i].n0);
+      continue;
+    }
+    grid_at.emplace(tasks[i]->fn, tc[r].init_off);
     for (uint64_t cell = 0; cell < ht[i].n0; ++cell) {
       double* lo = c.h_rects + tc[r].init_off + 2 * D * cell;
       double* hi = lo + D;
@@ -361,6 +388,8 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
       (!hp.consts.empty() && (e = up(c.buf.consts, hp.consts.data(), sizeof(double) * hp.consts.size())) != cudaSuccess))
     return cuda_fail(e, "cudaMemcpyAsync(tree setup)");
   prepare_programs(hp, false);
+  const auto t_setup = tclk::now();
+  int rounds = 0;
   std::vector<uint64_t> gt(2 * hp.groups.size());
   for (int round = 0;; ++round) {
     if (round > 0 && (e = launch_tree_select(c.t_const, c.t_state, L, uint32_t(T), s)) != cudaSuccess)
@@ -375,6 +404,7 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     uint64_t tiles = 0;
     for (size_t g = 0; g < hp.groups.size(); ++g) tiles += gt[2 * g + 1];
     if (tiles == 0) break;
+    ++rounds;
     if ((e = launch_expand_tiles(c.buf.fns, uint32_t(T), 1, c.buf.tile_fn, s)) != cudaSuccess)
       return cuda_fail(e, "launch k_expand_tiles");
     for (size_t g = 0; g < hp.groups.size(); ++g) {
@@ -390,6 +420,11 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     if ((e = launch_combine(c.buf.fns, uint32_t(T), 1, c.buf.part, c.buf.out, s)) != cudaSuccess ||
         (e = launch_tree_scatter(c.t_const, c.t_state, L, uint32_t(T), s)) != cudaSuccess)
       return cuda_fail(e, "launch tree combine/scatter");
+  }
+  if (trace) {
+    auto ms = [](tclk::time_point a, tclk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[mcb tree/dev %d] %zu trees: host setup %.3f ms, %d rounds %.3f ms\n", device, T,
+                 ms(t_start, t_setup), rounds, ms(t_setup, tclk::now()));
   }
   if ((e = launch_tree_finish(c.t_const, c.t_state, L, uint32_t(T), c.buf.out, s)) != cudaSuccess)
     return cuda_fail(e, "launch k_tree_finish");
