@@ -365,13 +365,23 @@ def tree_refine(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, de
     Returns the TrialStats, or (TrialStats, [Leaf]) with ``leaves=True``."""
     st = TrialStats()
     n = ctypes.c_size_t()
-    _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), None, 0,
-                               ctypes.byref(n)))
     if not leaves:
+        _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), None, 0,
+                                   ctypes.byref(n)))
         return st
-    buf = (Leaf * max(1, n.value))()
-    _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), buf,
-                               n.value, ctypes.byref(n)))
+    # one call when the leaves fit the bound (first pass <= 4096 cells or the
+    # given grid, plus one leaf per affordable split); the tree runs again only
+    # if they do not
+    spc = max(2, f.samples_per_cell if f.flags & FLAG_REFINE_CONFIG else 2048)
+    grid = f.cells_per_dim ** f.dim if f.cells_per_dim else 4096
+    cap = int(min(1 << 22, grid + f.n_samples // spc + 1))
+    buf = (Leaf * cap)()
+    _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), buf, cap,
+                               ctypes.byref(n)))
+    if n.value > cap:
+        buf = (Leaf * n.value)()
+        _check(lib.mcb_tree_refine(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st), buf,
+                                   n.value, ctypes.byref(n)))
     return st, list(buf[:n.value])
 
 
@@ -380,11 +390,14 @@ def stratified_mc(f: Integrand, cells_per_dim: int, samples_per_cell: int, seed:
     """stratified_mc (ref src/estimator.cpp:161-182) on the GPU: (TrialStats, [Leaf])."""
     st = TrialStats()
     n = ctypes.c_size_t()
+    cap = int(min(1 << 22, max(1, cells_per_dim) ** f.dim))
+    buf = (Leaf * cap)()
     _check(lib.mcb_stratified_mc(ctypes.byref(f), cells_per_dim, samples_per_cell, cell_cap, seed, trial,
-                                 chunk_base, device, ctypes.byref(st), None, 0, ctypes.byref(n)))
-    buf = (Leaf * max(1, n.value))()
-    _check(lib.mcb_stratified_mc(ctypes.byref(f), cells_per_dim, samples_per_cell, cell_cap, seed, trial,
-                                 chunk_base, device, ctypes.byref(st), buf, n.value, ctypes.byref(n)))
+                                 chunk_base, device, ctypes.byref(st), buf, cap, ctypes.byref(n)))
+    if n.value > cap:
+        buf = (Leaf * n.value)()
+        _check(lib.mcb_stratified_mc(ctypes.byref(f), cells_per_dim, samples_per_cell, cell_cap, seed, trial,
+                                     chunk_base, device, ctypes.byref(st), buf, n.value, ctypes.byref(n)))
     return st, list(buf[:n.value])
 
 
