@@ -356,12 +356,21 @@ McEstimate tree_refine(const IntegrandSpec& spec, const RefineConfig& config, co
   d.n_samples = config.total_budget;
   mcb_trial_stats st{};
   size_t n = 0;
+  std::vector<mcb_leaf> lv;
+  if (leaves_out) {  // leaf bound: first pass (<= 4096 cells, or the given grid) + one per split
+    double grid = 4096.0;
+    if (config.init_cells_per_dim) grid = std::pow(double(config.init_cells_per_dim), double(s.dim));
+    lv.resize(size_t(std::min(double(1 << 22),
+                              grid + double(config.total_budget / std::max<uint32_t>(config.samples_per_cell, 2)) + 1)));
+  }
   check(mcb_tree_refine(&d, key_base.global_seed, key_base.trial_index, key_base.chunk_index, device, &st,
-                        nullptr, 0, &n));
-  std::vector<mcb_leaf> lv(n);
-  if (leaves_out)
+                        lv.empty() ? nullptr : lv.data(), lv.size(), &n));
+  if (leaves_out && n > lv.size()) {  // past the bound: run again with room for every leaf
+    lv.resize(n);
     check(mcb_tree_refine(&d, key_base.global_seed, key_base.trial_index, key_base.chunk_index, device, &st,
                           lv.data(), lv.size(), &n));
+  }
+  lv.resize(std::min(lv.size(), n));
   if (st.status == MCB_TRIAL_CELL_BUDGET) throw CellBudgetExceeded("cell grid exceeds configured cap");
   if (st.status == MCB_TRIAL_CHUNK_RANGE) throw std::out_of_range("chunk_index exceeds 32 bits");
   if (st.status == MCB_TRIAL_ALL_NONFINITE)
@@ -394,12 +403,15 @@ std::pair<McEstimate, std::vector<StratumNode>> stratified_mc(const IntegrandSpe
   mcb_integrand d = to_descriptor(s, key_base.integrand_index, prog);
   mcb_trial_stats st{};
   size_t n = 0;
+  std::vector<mcb_leaf> lv(size_t(std::min(double(1 << 22), std::pow(double(cells_per_dim), double(s.dim)))));
   check(mcb_stratified_mc(&d, cells_per_dim, samples_per_cell, cell_cap, key_base.global_seed,
-                          key_base.trial_index, key_base.chunk_index, device, &st, nullptr, 0, &n));
-  std::vector<mcb_leaf> lv(n);
-  if (n)
+                          key_base.trial_index, key_base.chunk_index, device, &st, lv.data(), lv.size(), &n));
+  if (n > lv.size()) {
+    lv.resize(n);
     check(mcb_stratified_mc(&d, cells_per_dim, samples_per_cell, cell_cap, key_base.global_seed,
                             key_base.trial_index, key_base.chunk_index, device, &st, lv.data(), lv.size(), &n));
+  }
+  lv.resize(std::min(lv.size(), n));
   if (st.status == MCB_TRIAL_CELL_BUDGET) throw CellBudgetExceeded("cell grid exceeds configured cap");
   if (st.status == MCB_TRIAL_CHUNK_RANGE) throw std::out_of_range("chunk_index exceeds 32 bits");
   if (st.status != MCB_TRIAL_OK) throw AllSamplesNonFinite("every sample evaluated to NaN or infinity");
