@@ -320,13 +320,32 @@ def run_mcb_arm(args, dist, local):
                      "note": "achieved = Philox4x32-10 blocks per launch (2 per 4-D sample) / k_direct "
                              "time; peak = mcb_probe_philox_peak (Philox-only, same code, measured live); "
                              "traffic = dram__bytes_read+write of this k_direct launch from " + NCU_SUMMARY +
-                             " (tile table + descriptors; the kernel is ALU-bound)"},
+                             " (tile table + descriptors; the kernel is ALU-bound, SURVEY.md §8(d))",
+                     "hbm": hbm_roofline(ncu_traffic(), kernel_s / args.steps)},
         "clocks": clk.summary(),
     }
     return line
 
 
 NCU_SUMMARY = "profiles/r01_bench_k_direct_ncu_summary.txt"
+
+
+def hbm_roofline(traffic_bytes, launch_s):
+    """The HBM roofline of the same launch, for reference: measured DRAM bytes
+    over the launch time against MEASURED_PEAKS.json's copy bandwidth (the
+    schema's "hbm" bound; ~1e-6 here — the kernel is compute-bound)."""
+    if traffic_bytes is None or launch_s <= 0:
+        return None
+    peak = None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+        source = "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        peak, source = 7700.0, "B200_PROFILING.md nominal"
+    achieved = traffic_bytes / launch_s / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic_bytes, "peak_source": source}
 
 
 def ncu_traffic():
