@@ -166,6 +166,7 @@ uint64_t splitmix64(uint64_t z);
 uint64_t chunk_count(uint64_t n);
 bool cell_grid_size(uint32_t k, uint32_t d, uint64_t cap, uint64_t& cells);
 uint32_t auto_cells_per_dim(uint32_t d, uint64_t limit);
+uint32_t int_root_floor(uint64_t x, uint32_t d);
 StratPlan stratified_plan(const mcb_integrand& f);
 bool stratified(const mcb_integrand& f);
 uint64_t trial_samples(const mcb_integrand& f);

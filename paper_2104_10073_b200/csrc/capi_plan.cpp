@@ -59,19 +59,30 @@ bool cell_grid_size(uint32_t k, uint32_t d, uint64_t cap, uint64_t& cells) {
   return cells <= cap;
 }
 
-// auto_cells_per_dim: the largest k with k^d <= limit (at least 1).
-uint32_t auto_cells_per_dim(uint32_t d, uint64_t limit) {
-  uint32_t k = 1;
-  for (;;) {
-    uint64_t cells = 1;
-    for (uint32_t i = 0; i < d; ++i) {
-      cells *= uint64_t(k) + 1;
-      if (cells > limit) return k;
-    }
-    ++k;
+// k^d, saturating at UINT64_MAX.
+static uint64_t sat_pow(uint64_t k, uint32_t d) {
+  uint64_t r = 1;
+  for (uint32_t i = 0; i < d; ++i) {
+    if (k && r > UINT64_MAX / k) return UINT64_MAX;
+    r *= k;
   }
+  return r;
 }
 
+// The largest k >= 1 with k^d <= x (1 when there is none): a floating-point
+// guess corrected with exact integer powers.
+uint32_t int_root_floor(uint64_t x, uint32_t d) {
+  if (d == 0 || x <= 1) return 1;
+  uint64_t k = uint64_t(std::pow(double(x), 1.0 / d));
+  k = std::min<uint64_t>(std::max<uint64_t>(k, 1), 0xFFFFFFFFull);
+  while (k > 1 && sat_pow(k, d) > x) --k;
+  while (k < 0xFFFFFFFFull && sat_pow(k + 1, d) <= x) ++k;
+  return uint32_t(k);
+}
+
+// auto_cells_per_dim (src/estimator.cpp:107-122): the largest k with
+// k^d <= limit (at least 1) — the reference's k = 1, 2, ... search, closed form.
+uint32_t auto_cells_per_dim(uint32_t d, uint64_t limit) { return int_root_floor(limit, d); }
 
 StratPlan stratified_plan(const mcb_integrand& f) {
   StratPlan p;

@@ -164,12 +164,15 @@ bool tree_first_pass(const mcb_integrand& f, const mcb::tree::Config& cfg, uint3
                      uint64_t& n0) {
   k = cfg.init_cells_per_dim;
   if (k == 0) {
+    // the reference steps k down from the automatic size until the grid
+    // takes at most half the budget (stopping at 1), every step through the
+    // cell cap; k^d falls with k, so only the first step can hit the cap and
+    // the stop is the largest k with k^d <= (budget/2)/spc
     k = auto_cells_per_dim(f.dim, 4096);
-    while (k > 1) {
+    if (k > 1) {
       uint64_t cells;
       if (!cell_grid_size(k, f.dim, cfg.cell_cap, cells)) return false;
-      if (cells * spc <= cfg.total_budget / 2) break;
-      --k;
+      k = std::min(k, int_root_floor(cfg.total_budget / 2 / spc, f.dim));
     }
   }
   return cell_grid_size(k, f.dim, cfg.cell_cap, n0);
@@ -241,6 +244,7 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     h.prep = prepare(f, seed, 0, tasks[i]->trial, true);
     if (h.spc <= kWarpTileMaxSpc) h.prep.variant |= kWarpTile;
   }
+  const auto t_cfg = tclk::now();
   std::vector<size_t> order(T);  // launch groups: (family, dim, variant, program)
   std::iota(order.begin(), order.end(), size_t(0));
   auto key = [&](size_t i) {
@@ -315,31 +319,34 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     if (g.family != MCB_FAMILY_PROGRAM && !variant_supported(g.family, g.dim, g.variant))
       return fail(MCB_ERR_INVALID_ARGUMENT, "unsupported (family, dim) combination");
   // first-pass grids (grid_cell, src/estimator.cpp:124-143) = the initial
-  // leaves and round-0 cells, packed tree after tree (k_tree_init spreads them)
+  // leaves and round-0 cells: one packed grid per integrand (its trials share
+  // it), k_tree_init spreads them into every tree's storage
   uint64_t packed_doubles = 0;
+  std::map<const mcb_integrand*, uint64_t> grid_at;  // packed offset of an integrand's grid
+  std::vector<size_t> grid_rows;                      // one tree per distinct grid
   for (size_t r = 0; r < T; ++r) {
-    tc[r].init_off = packed_doubles;
-    packed_doubles += uint64_t(tst[r].n_leaves) * 2 * tc[r].dim;
+    tc[r].init_off = 0;
+    if (tst[r].n_leaves == 0) continue;  // failed before the first pass
+    auto it = grid_at.find(tasks[order[r]]->fn);
+    if (it == grid_at.end()) {
+      it = grid_at.emplace(tasks[order[r]]->fn, packed_doubles).first;
+      packed_doubles += uint64_t(tst[r].n_leaves) * 2 * tc[r].dim;
+      grid_rows.push_back(r);
+    }
+    tc[r].init_off = it->second;
   }
+  const auto t_desc = tclk::now();
   DeviceCtx& c = device_ctx(device);
   std::lock_guard<std::mutex> lock(c.mu);
   DeviceGuard guard(device);
   cudaError_t e;
   if ((e = grow_pinned(c.h_rects, c.h_rects_cap, packed_doubles)) != cudaSuccess)
     return cuda_fail(e, "cudaMallocHost");
-  std::map<const mcb_integrand*, uint64_t> grid_at;  // packed offset of an integrand's grid
-  for (size_t r = 0; r < T; ++r) {
+  for (size_t r : grid_rows) {
     const size_t i = order[r];
     const mcb_integrand& f = *tasks[i]->fn;
     const uint32_t k = ht[i].k, D = f.dim;
-    if (ht[i].n0 == 0) continue;
-    auto done = grid_at.find(tasks[i]->fn);
-    if (done != grid_at.end()) {  // another trial of the same integrand: same grid
-      std::memcpy(c.h_rects + tc[r].init_off, c.h_rects + done->second, sizeof(double) * 2 * D * ht[i].n0);
-      continue;
-    }
-    grid_at.emplace(tasks[i]->fn, tc[r].init_off);
-    for (uint64_t cell = 0; cell < ht[i].n0; ++cell) {
+    for (uint64_t cell = 0; cell < tst[r].n_leaves; ++cell) {
       double* lo = c.h_rects + tc[r].init_off + 2 * D * cell;
       double* hi = lo + D;
       uint64_t rem = cell;
@@ -352,6 +359,7 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
       }
     }
   }
+  const auto t_grid = tclk::now();
   // ---- device ----
   if (!c.ready) {
     if ((e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking)) != cudaSuccess)
@@ -423,8 +431,11 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
   }
   if (trace) {
     auto ms = [](tclk::time_point a, tclk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    std::fprintf(stderr, "[mcb tree/dev %d] %zu trees: host setup %.3f ms, %d rounds %.3f ms\n", device, T,
-                 ms(t_start, t_setup), rounds, ms(t_setup, tclk::now()));
+    std::fprintf(stderr,
+                 "[mcb tree/dev %d] %zu trees: host setup %.3f ms (configs %.3f, descriptors %.3f, grids %.3f, "
+                 "uploads %.3f), %d rounds %.3f ms\n",
+                 device, T, ms(t_start, t_setup), ms(t_start, t_cfg), ms(t_cfg, t_desc), ms(t_desc, t_grid),
+                 ms(t_grid, t_setup), rounds, ms(t_setup, tclk::now()));
   }
   if ((e = launch_tree_finish(c.t_const, c.t_state, L, uint32_t(T), c.buf.out, s)) != cudaSuccess)
     return cuda_fail(e, "launch k_tree_finish");
@@ -556,13 +567,18 @@ mcb_status run_trees_on(std::vector<mcb::tree::TreeTask>& tasks, uint64_t seed, 
   }
   // leaf storage is reserved up front on the device: very large trees (a
   // budget / depth allowing > 64 Mi leaves in one call) take the host driver
-  uint64_t bound = 0;
-  for (auto& t : tasks) {
-    const mcb::tree::Config cfg = mcb::tree::config_of(*t.fn);
-    const uint32_t spc = std::max<uint32_t>(cfg.samples_per_cell, 2);
-    uint32_t k;
-    uint64_t n0;
-    if (tree_first_pass(*t.fn, cfg, spc, k, n0)) bound += tree_leaf_bound(n0, spc, cfg);
+  uint64_t bound = 0, last = 0;
+  const mcb_integrand* last_fn = nullptr;
+  for (auto& t : tasks) {  // the trials of an integrand are adjacent: one bound each
+    if (t.fn != last_fn) {
+      const mcb::tree::Config cfg = mcb::tree::config_of(*t.fn);
+      const uint32_t spc = std::max<uint32_t>(cfg.samples_per_cell, 2);
+      uint32_t k;
+      uint64_t n0;
+      last = tree_first_pass(*t.fn, cfg, spc, k, n0) ? tree_leaf_bound(n0, spc, cfg) : 0;
+      last_fn = t.fn;
+    }
+    bound += last;
   }
   if (bound > (uint64_t(1) << 26)) {
     std::mutex err_mu;

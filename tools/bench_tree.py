@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Throughput of the tree method end to end through
 mcb_run_direct: host refinement rounds + per-round batched cell launches.
-Reports samples actually drawn per second (the trees stop below their budget
-when no leaf stands out), rounds, and the reference's own CPU run_batch on a
+Reports the reference's n_samples (spc per final leaf) per second — the trees
+stop below their budget when no leaf stands out — and the samples the kernels
+actually draw (split parents included), and the reference's own CPU run_batch on a
 bounded sample of the same trees (oracle/_ref, all host threads) when present.
 
   python tools/bench_tree.py [--fns 200] [--trials 10] [--budget 1000000] [--ref-fns 8]
@@ -56,9 +57,18 @@ def main():
         times.append(time.perf_counter() - t0)
     t = min(times)
     drawn = int(out["n_samples"].sum())
+    # n_samples is the reference's count (spc per final leaf); a split re-samples
+    # both halves, so the kernels draw (n_leaves - n0) * spc more per tree.  n0
+    # (first-pass cells) from one tree's leaves: each first-pass cell is a full
+    # binary tree, so sum(2^-depth) over its leaves is 1 (same config for all).
+    _, leaves = mcb.tree_refine(fns[0], seed, 0, leaves=True)
+    n0 = round(sum(2.0 ** -l.depth for l in leaves))
+    actual = drawn + int((out["n_cells"].astype(np.int64) - n0).sum()) * args.spc
     res = {"workload": f"{args.fns} {args.integrand} trees x {args.trials} trials, budget {args.budget}, "
                        f"spc {args.spc}",
            "seconds": t, "samples_drawn": drawn, "samples_per_s": drawn / t,
+           "first_pass_cells": n0, "samples_drawn_incl_split_parents": actual,
+           "kernel_samples_per_s": actual / t,
            "leaves_mean": float(out["n_cells"].mean()), "max_depth": int(out["max_depth"].max()),
            "budget_exhausted": int(out["budget_exhausted"].sum()),
            "ok": int((out["status"] == mcb.TRIAL_OK).sum())}
