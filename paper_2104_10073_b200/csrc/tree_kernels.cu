@@ -42,10 +42,16 @@ template <class G>
 __device__ __forceinline__ double warp_ordered_sum(uint32_t n, G g) {
   const uint32_t lane = threadIdx.x & 31;
   double acc = 0.0;
+  double v = lane < n ? g(lane) : 0.0;
   for (uint32_t base = 0; base < n; base += 32) {
-    const double v = base + lane < n ? g(base + lane) : 0.0;
+    const double next = base + 32 + lane < n ? g(base + 32 + lane) : 0.0;  // in flight during the chain
     const uint32_t m = min(32u, n - base);
-    for (uint32_t j = 0; j < m; ++j) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, j));
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j) {  // unrolled: the shuffles run ahead of the add chain
+      const double x = __shfl_sync(0xffffffffu, v, j);
+      if (j < m) acc = __dadd_rn(acc, x);
+    }
+    v = next;
   }
   return acc;
 }
