@@ -14,7 +14,8 @@
 //   * the sample coordinates likewise, X[j][h][tid].
 // Every operation is the reference's: IEEE +,-,*,/ (correctly rounded, as
 // on the host), libdevice sin/cos/tan/asin/acos/atan/exp/log/pow (<= 2 ulp of
-// glibc), exact sqrt/fabs/floor/fmin/fmax.  Points are the same bit-exact
+// glibc), exact sqrt/fabs/floor/fmin/fmax, and the fused cos + sin of one
+// argument in the Fig. 1 table form (dev::cos_plus_sin).  Points are the same bit-exact
 // Philox stream; non-finite values are counted and skipped.
 #include <cuda_runtime.h>
 
@@ -93,6 +94,7 @@ __device__ __forceinline__ void interp_pair(const uint32_t* __restrict__ code, u
       case prog::kFloor: r0 = floor(a0); r1 = floor(a1); break;
       case prog::kMin: r0 = fmin(a0, b0); r1 = fmin(a1, b1); break;
       case prog::kMax: r0 = fmax(a0, b0); r1 = fmax(a1, b1); break;
+      case prog::kCosPlusSin: r0 = dev::cos_plus_sin(a0); r1 = dev::cos_plus_sin(a1); break;
       default: r0 = r1 = __longlong_as_double(0x7FF8000000000000ll); break;
     }
     double* d = S + ((w0 >> 8) & 31u) * 2 * T + tid;

@@ -418,6 +418,47 @@ struct Scheduler {
   }
 };
 
+// Reads of every internal node reachable from `root` (one per operand
+// position of each reachable parent, plus one for the root).
+std::vector<int> reads_of(const std::vector<DagNode>& nodes, int root) {
+  std::vector<int> reads(nodes.size(), 0);
+  std::vector<bool> seen(nodes.size(), false);
+  std::vector<int> stack{root};
+  while (!stack.empty()) {
+    const int id = stack.back();
+    stack.pop_back();
+    if (seen[size_t(id)]) continue;
+    seen[size_t(id)] = true;
+    const DagNode& n = nodes[size_t(id)];
+    if (n.leaf) continue;
+    ++reads[size_t(n.a)];
+    stack.push_back(n.a);
+    if (n.b >= 0) {
+      ++reads[size_t(n.b)];
+      stack.push_back(n.b);
+    }
+  }
+  ++reads[size_t(root)];
+  return reads;
+}
+
+// cos(E) + sin(E) / sin(E) + cos(E), each call read only by that sum, into
+// one kCosPlusSin(E) (IEEE addition is commutative, so both orders are the
+// reference's cos + sin).
+void fuse_cos_plus_sin(std::vector<DagNode>& nodes, int root) {
+  const std::vector<int> reads = reads_of(nodes, root);
+  for (size_t id = 0; id < nodes.size(); ++id) {
+    DagNode& n = nodes[id];
+    if (!reads[id] || n.leaf || n.op != kAdd || n.b < 0) continue;
+    const DagNode &l = nodes[size_t(n.a)], &r = nodes[size_t(n.b)];
+    if (l.leaf || r.leaf || l.a != r.a || reads[size_t(n.a)] != 1 || reads[size_t(n.b)] != 1) continue;
+    if (!((l.op == kCos && r.op == kSin) || (l.op == kSin && r.op == kCos))) continue;
+    n.op = kCosPlusSin;
+    n.a = l.a;
+    n.b = -1;
+  }
+}
+
 }  // namespace
 
 std::vector<uint32_t> Program::words() const {
@@ -444,6 +485,7 @@ Program compile(const std::string& source, uint32_t dim,
     throw CompileError("more than " + std::to_string(kMaxParams) + " parameters");
   Lowering lw{p, {}, {}, {}};
   const int root = lw.lower(*root_tree);
+  fuse_cos_plus_sin(lw.nodes, root);
   const auto& nodes = lw.nodes;
   Scheduler sc{p, nodes, std::vector<int>(nodes.size(), 0), std::vector<int>(nodes.size(), -1),
                std::vector<int>(nodes.size(), -1), {}};
@@ -530,6 +572,7 @@ double evaluate(const Program& p, const double* x, const double* params) {
       case kFloor: r = std::floor(a); break;
       case kMin: r = std::fmin(a, b); break;
       case kMax: r = std::fmax(a, b); break;
+      case kCosPlusSin: r = std::cos(a) + std::sin(a); break;
       default: break;
     }
     st[i.dst] = r;
@@ -579,6 +622,7 @@ std::string emit_cuda(const Program& p, const std::string& name) {
       case kPow: o += "    " + d + " = pow(" + a + ", " + b + ");\n"; break;
       case kMin: o += "    " + d + " = fmin(" + a + ", " + b + ");\n"; break;
       case kMax: o += "    " + d + " = fmax(" + a + ", " + b + ");\n"; break;
+      case kCosPlusSin: o += "    " + d + " = mcb::dev::cos_plus_sin(" + a + ");\n"; break;
       default:
         if (i.op < kNumOps && i.op < sizeof(unary) / sizeof(unary[0]) && unary[i.op])
           o += "    " + d + " = " + unary[i.op] + "(" + a + ");\n";

@@ -20,9 +20,12 @@
 // function of its operands), sin/cos of the same argument fuse into one
 // sincos, leaves become operand modes (slot | variable | constant |
 // parameter) instead of load instructions, and values live in a small set
-// of register slots freed at their last use.  The Fig. 1 integrand
-// cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4)) is 21 postfix instructions in
-// the reference and 6 here.
+// of register slots freed at their last use.  `cos(E) + sin(E)` (either
+// order, the two calls used nowhere else) becomes one cos_plus_sin(E): the
+// Fig. 1 family's table form on the device (mcb_device.cuh), whose error,
+// <= 2 ulp of 1, is that of the reference's two rounded libm values and
+// rounded add.  The Fig. 1 integrand cos(k*(x1+x2+x3+x4)) +
+// sin(k*(x1+x2+x3+x4)) is 21 postfix instructions in the reference and 5 here.
 #pragma once
 
 #include <cstdint>
@@ -55,6 +58,7 @@ enum Op : uint8_t {
   kFloor,
   kMin,
   kMax,
+  kCosPlusSin,  // dst = cos(a) + sin(a): the compiler's fusion of `cos(E) + sin(E)`
   kNumOps
 };
 

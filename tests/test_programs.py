@@ -83,10 +83,10 @@ def test_oracle_estimates_match_reference(progs, oracle):
 def test_compiler_contract(mcb):
     p = mcb.Program("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, ["k"])
     # reference postfix: 21 instructions, stack 4; the GPU
-    # form shares k*(x1+..+x4), fuses sin/cos into one sincos and folds loads
-    # into operands: Add, Add, Add, Mul, SinCos, Add in 3 slots
+    # form shares k*(x1+..+x4), folds loads
+    # into operands and fuses cos(E) + sin(E): Add, Add, Add, Mul, CosPlusSin in 1 slot
     assert len(dsl.Program(p.source, 4, {"k": 1.0}).code) == 21
-    assert (p.n_instr, p.depth) == (6, 3)
+    assert (p.n_instr, p.depth) == (5, 1)
     assert mcb.Program("a*x1 + b + c", 1, ["c", "a", "b"]).param_names == ["a", "b", "c"]
     cases = {
         "x3": "x3 exceeds dim=2",
@@ -243,6 +243,42 @@ def test_random_programs_vs_oracle(gpu, oracle):
 
 
 @pytest.mark.gpu
+def test_cos_plus_sin_fusion(gpu):
+    """cos(E) + sin(E) runs as one fused op: the table form for |E| < 2^20,
+    libdevice beyond and for non-finite E.  Per-sample values within 4 ulp of 1
+    (absolute) of glibc's cos + sin on both sides of the switch (k = 3 keeps E
+    small, k = 1e7 crosses 2^20 inside [0, 1]), NaN where E is NaN, and the
+    runtime-specialised kernel bit-identical to the interpreter."""
+    n = 4000
+    cases = [("cos(k*x1) + sin(k*x1)", {"k": 3.0}), ("sin(k*x1) + cos(k*x1)", {"k": 1e7}),
+             ("cos(log(x1-0.5)) + sin(log(x1-0.5))", {})]
+    for i, (src, params) in enumerate(cases):
+        q = gpu.Program(src, 1, list(params))
+        assert q.n_instr <= 3, src  # fused: no separate sincos + add
+        f = q.integrand(params, n_samples=n, index=i)
+        got = gpu.debug_eval(f, 31, 0, 0, 0, n)
+        pts = _oracle.sample_uniform([0.0], [1.0], 31, i, 0, 0, 0, n)
+        want = np.array([dsl.Program(src, 1, params)(row) for row in pts])
+        bad = ~np.isfinite(want)
+        assert np.array_equal(~np.isfinite(got), bad), src
+        assert np.all(np.abs(got[~bad] - want[~bad]) <= 4 * 2.0 ** -52), (src, np.abs(got - want).max())
+        if params.get("k") == 1e7:
+            t = params["k"] * pts[:, 0]
+            assert (t < 2 ** 20).any() and (t >= 2 ** 20).any()
+    assert gpu.program_jit(2) == 2, gpu.program_jit_error()
+    fns = [gpu.Program(src, 1, list(params)) for src, params in cases]
+    ints = [p.integrand(params, n_samples=300_000, index=i) for i, (p, (_, params)) in enumerate(zip(fns, cases))]
+    try:
+        a = gpu.run_direct(ints, 5, 2)
+        assert gpu.program_jit_error() == "", gpu.program_jit_error()
+        gpu.program_jit(0)
+        b = gpu.run_direct(ints, 5, 2)
+    finally:
+        gpu.program_jit(1)
+    assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.gpu
 def test_jit_bit_identical_to_interpreter(gpu, progs):
     """Runtime-specialised programs (NVRTC, csrc/jit.cpp) against the bytecode
     interpreter: every per-trial McEstimate byte-identical, in all four modes
@@ -281,9 +317,11 @@ def test_jit_code_compiles_for_every_golden_program(mcb, progs, tmp_path, monkey
     monkeypatch.setenv("MCB_JIT_CACHE", str(tmp_path))
     srcs = [(c["source"], c["dim"], list(c["params"])) for c in progs[:3]]
     srcs += [("7", 1, []), ("1e308*1e308 - x1", 1, []), ("a+b+c+d+e2+f+g+h", 1, list("abcdfgh") + ["e2"])]
+    salt = f" + 0*x1*{os.getpid()}"  # a program no earlier test of this process compiled
     for src, dim, names in srcs:
-        p = mcb.Program(src, dim, names)
+        p = mcb.Program("(" + src + ")" + salt, dim, names)
         p.jit_build()
+        assert mcb.program_jit_error() == "", (src, mcb.program_jit_error())
     assert len(list(tmp_path.iterdir())) >= 4 * len(srcs)  # four kernel modes each, cached
 
 
