@@ -406,7 +406,17 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   if (!harm) p.variant &= ~kUnitCoef;
   if (strat) p.variant |= kStrat;
   if (tree_cells) p.variant &= ~kNoShift;  // cells shrink: keep the per-tile shift
-  if (stratified(f) && d.spc <= kWarpTileMaxSpc) p.variant |= kWarpTile;
+  if (stratified(f) && d.spc <= kWarpTileMaxSpc) {
+    // small cells: a lane per cell on large grids (unit-coefficient or no
+    // table), else a warp per cell
+    const bool general_table = harm && !(p.variant & kSafe) && !(p.variant & kUnitCoef);
+    if (d.n_cells >= kLaneCellMinCells && !general_table) {
+      p.variant |= kLaneCell;
+      d.n_chunks = round_up(d.n_cells * d.cpc, kLaneAlign);
+    } else {
+      p.variant |= kWarpTile;
+    }
+  }
   // shift constant: f at the domain midpoint (reference op order, libm);
   // cells use a per-tile shift computed on the device instead
   if (!strat) {
@@ -514,7 +524,7 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     const size_t i = order[r];
     FnDesc d = prep[i].d;
     const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
-    if (var & mcb::detail::kWarpTile) tile = round_up<uint64_t>(tile, mcb::detail::kTileAlign);
+    tile = round_up<uint64_t>(tile, mcb::detail::tiles_per_cta(var));
     d.tile_base = tile;
     d.out_slot = i;
     const uint64_t nt = uint64_t(d.n_chunks) * trials;

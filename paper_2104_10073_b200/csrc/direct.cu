@@ -298,7 +298,7 @@ static const Table& table() {
 
 static const Entry* entry(int family, int dim, int variant) {
   if (family < 0 || family > 3 || dim < 1 || dim > int(MCB_MAX_DIM) || variant < 0 ||
-      variant > 63)
+      variant >= kNumVariants)
     return nullptr;
   const Entry* e = &table().e[family][dim][variant];
   return e->direct ? e : nullptr;
@@ -312,12 +312,13 @@ cudaError_t launch_direct_group(const GroupLaunch& g, const FnDesc* fns, const u
                                 TilePartial* part, cudaStream_t s) {
   const Entry* e = entry(g.family, g.dim, g.variant);
   if (!e) return cudaErrorInvalidValue;
-  const uint64_t per_cta = (g.variant & kWarpTile) ? uint64_t(kTileAlign) : 1u;  // tiles per CTA
+  const uint64_t per_cta = tiles_per_cta(g.variant);
+  const uint32_t threads = (g.variant & kLaneCell) ? kLaneAlign : kThreads;
   const uint64_t n_ctas = g.n_tiles / per_cta;
   const uint64_t kMaxGrid = 0x7FFFFFF8ull;
   for (uint64_t off = 0; off < n_ctas; off += kMaxGrid) {
     const uint64_t n = n_ctas - off < kMaxGrid ? n_ctas - off : kMaxGrid;
-    e->direct<<<dim3(uint32_t(n)), dim3(kThreads), 0, s>>>(fns, tile_fn, g.tile0 + off * per_cta, part);
+    e->direct<<<dim3(uint32_t(n)), dim3(threads), 0, s>>>(fns, tile_fn, g.tile0 + off * per_cta, part);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }

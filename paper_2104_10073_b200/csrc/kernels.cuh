@@ -294,6 +294,96 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
   }
 }
 
+// K3l k_direct_lane<FAM,D,V> (V has kStrat | kLaneCell): the small cells of a
+// large stratified grid (one chunk per cell), one LANE per cell.  A one-warp
+// CTA covers kLaneAlign consecutive cells of one (integrand, trial) (ranges
+// padded / aligned by the host), so the descriptor is CTA-uniform; each lane
+// runs its cell start to finish like a K3 thread runs its pairs — sample 0 is
+// the cell's shift, the pairs in ascending order, two per iteration — and
+// writes the cell's TilePartial: no shuffles, no reduction, no idle lanes on
+// a partial last round of pairs.  Tables: unit coefficients (read through
+// L1) or none (SAFE / abs); the host keeps general-coefficient harmonic
+// grids on K3w.
+template <int FAM, int D, int V>
+__global__ void __launch_bounds__(kLaneAlign, 8 * warp_tile_min_blocks(D, V))
+    k_direct_lane(const FnDesc* __restrict__ fns, const uint32_t* __restrict__ tile_fn, uint64_t tile0,
+                  TilePartial* __restrict__ part) {
+  constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
+  constexpr bool SAFE = (V & kSafe) != 0;
+  constexpr bool NOSHIFT = (V & kNoShift) != 0;
+  constexpr bool HARM = FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC;
+  constexpr bool TABLE = HARM && !SAFE;
+  static_assert((V & kStrat) && (V & kLaneCell) && !(V & kWarpTile), "cell-per-lane variant");
+  static_assert(!TABLE || UNIT_COEF, "general-coefficient tables stay on K3w");
+
+  const uint64_t group = tile0 + uint64_t(blockIdx.x) * kLaneAlign;
+  const uint32_t fi = __ldg(tile_fn + group);
+  FnDesc f = fns[fi];
+  const TrigAB* ab = TABLE ? dev::g_trig_unit_ab : nullptr;
+  const uint64_t tile = group + threadIdx.x;
+  const uint32_t rem = uint32_t(tile - f.tile_base);
+  const uint32_t trial = rem / f.n_chunks;
+  const uint32_t cell = rem - trial * f.n_chunks;  // one chunk per cell
+  if (cell >= f.n_cells) return;                   // padding lane of the aligned range
+  const uint32_t count = f.spc;
+  dev::cell_rect<D>(f, cell, SAFE ? 1.0 : dev::kTwoM64);
+  const uint32_t pairs = (count + 1) >> 1;
+  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + cell, f.trial_base + trial);
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t nbad = 0;
+  auto add = [&](uint32_t q, double f0, double f1) {
+    const bool has1 = 2 * q + 1 < count;
+    double g0 = NOSHIFT ? f0 : __dsub_rn(f0, f.shift);
+    double g1 = NOSHIFT ? f1 : __dsub_rn(f1, f.shift);
+    if (SAFE) {
+      const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
+      nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+      g0 = ok0 ? g0 : 0.0;
+      g1 = ok1 ? g1 : 0.0;
+    } else {
+      g1 = has1 ? g1 : 0.0;
+    }
+    s1 = __dadd_rn(s1, g0);
+    s2 = fma(g0, g0, s2);
+    s1 = __dadd_rn(s1, g1);
+    s2 = fma(g1, g1, s2);
+  };
+  constexpr uint64_t kStep = uint64_t(dev::kM0) * uint64_t(D);  // round-1 product step per pair
+  {  // pair 0: its first sample is the cell's shift
+    double x0, x1;
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, 0, x0, x1);
+    const double f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
+    const double f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
+    if (!NOSHIFT) f.shift = finite64(f0) ? f0 : 0.0;
+    add(0, f0, f1);
+  }
+  uint32_t q = 1;
+  uint64_t pq = kStep;
+  for (; q + 1 < pairs; q += 2, pq += 2 * kStep) {  // two independent chains per iteration
+    double x0, x1, y0, y1;
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, pq, x0, x1);
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, pq + kStep, y0, y1);
+    const double a0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
+    const double a1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
+    const double b0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, y0);
+    const double b1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, y1);
+    add(q, a0, a1);
+    add(q + 1, b0, b1);
+  }
+  if (q < pairs) {
+    double x0, x1;
+    dev::gen_pair<FAM, D, false, SAFE>(f, P, pq, x0, x1);
+    add(q, dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0), dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1));
+  }
+  TilePartial p;
+  p.s1 = s1;
+  p.s2 = s2;
+  p.shift = NOSHIFT ? 0.0 : f.shift;
+  p.n_nonfinite = SAFE ? nbad : 0u;
+  p.n_finite = count - p.n_nonfinite;
+  part[tile] = p;
+}
+
 // Family values of the pairs [first_pair, first_pair + n_pairs) of one chunk,
 // through exactly the gen_pair/finish instantiation the fused kernel uses.
 template <int FAM, int D, int V>
@@ -330,7 +420,7 @@ struct Entry {
 };
 
 struct Table {
-  Entry e[4][MCB_MAX_DIM + 1][64];
+  Entry e[4][MCB_MAX_DIM + 1][kNumVariants];
   template <int FAM, int D, int V>
   void put() {
     e[FAM][D][V].direct = k_direct<FAM, D, V>;
@@ -342,6 +432,9 @@ struct Table {
   void put_run() {
     e[FAM][D][V | kStrat].direct = k_direct<FAM, D, V | kStrat>;
     e[FAM][D][V | kStrat | kWarpTile].direct = k_direct_warp<FAM, D, V | kStrat | kWarpTile>;
+    constexpr bool TABLE = (FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC) && !(V & kSafe);
+    if constexpr (!TABLE || (V & kUnitCoef))
+      e[FAM][D][V | kStrat | kLaneCell].direct = k_direct_lane<FAM, D, V | kStrat | kLaneCell>;
   }
 };
 

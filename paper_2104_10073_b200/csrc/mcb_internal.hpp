@@ -38,17 +38,30 @@ enum Variant : int {
                     // integrand far from constant, so no cancellation)
   kStrat = 16,      // STRATIFIED method: tiles are (trial, cell, chunk), the
                     // cell rectangle is derived on the device (grid_cell)
-  kWarpTile = 32    // with kStrat, small cells: one WARP per tile, so a CTA
+  kWarpTile = 32,   // with kStrat, small cells: one WARP per tile, so a CTA
                     // covers kTileAlign tiles of one (integrand, trial); each
                     // integrand's per-trial tile range is padded to a
                     // multiple of kTileAlign and its tile_base aligned
+  kLaneCell = 64    // with kStrat (not kWarpTile), small cells of a large
+                    // grid: one LANE per cell, a one-warp CTA covers
+                    // kLaneAlign cells of one (integrand, trial); ranges
+                    // padded / aligned to kLaneAlign (family kernels only)
 };
+constexpr int kNumVariants = 128;
 
 // Tile alignment of kWarpTile integrands (= warps of the family kernel's CTA,
 // a multiple of the interpreter's 4 warps) and the cell size up to which
 // cell-structured integrands use it.
 constexpr uint32_t kTileAlign = 8;
 constexpr uint32_t kWarpTileMaxSpc = 8192;
+// kLaneCell: cells per CTA (one warp) and the smallest grid that uses it.
+constexpr uint32_t kLaneAlign = 32;
+constexpr uint32_t kLaneCellMinCells = 256;
+
+// Tiles per CTA and tile-range alignment of a variant's kernel.
+constexpr uint32_t tiles_per_cta(int variant) {
+  return (variant & kLaneCell) ? kLaneAlign : (variant & kWarpTile) ? kTileAlign : 1u;
+}
 static_assert(kThreads / 32 == int(kTileAlign), "family CTA = kTileAlign warps");
 static_assert(kTileAlign % (kProgThreads / 32) == 0, "interpreter CTAs tile the aligned groups");
 
