@@ -318,9 +318,7 @@ mcb_status mcb_plan_get_info(const mcb_plan* plan, mcb_plan_info* info) {
   info->philox_blocks = plan->hp.philox_blocks;
   uint32_t launches = 1;  // k_combine
   for (const auto& g : plan->hp.groups) {
-    const uint64_t ctas = g.n_tiles / ((g.family == MCB_FAMILY_PROGRAM && (g.variant & mcb::detail::kWarpTile))
-                                           ? uint64_t(mcb::detail::kProgThreads / 32)
-                                           : uint64_t(mcb::detail::tiles_per_cta(g.variant)));
+    const uint64_t ctas = g.n_tiles / mcb::detail::tiles_per_cta(g.variant, g.family == MCB_FAMILY_PROGRAM);
     launches += uint32_t((ctas + 0x7FFFFFF7ull) / 0x7FFFFFF8ull);
   }
   info->launches_per_run = launches;

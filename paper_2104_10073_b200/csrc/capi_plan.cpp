@@ -347,7 +347,14 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
     // interpreter: plain parameters, unscaled draws, non-finite counting
     for (uint32_t j = 0; j < MCB_MAX_DIM; ++j) d.k[j] = f.k[j];
     p.variant = kSafe | (unit_dom ? kUnitDomain : 0) | (strat ? kStrat : 0);
-    if (stratified(f) && d.spc <= kWarpTileMaxSpc) p.variant |= kWarpTile;
+    if (stratified(f) && d.spc <= kWarpTileMaxSpc) {  // small cells: lane per cell on large grids
+      if (d.n_cells >= kProgLaneMinCells) {
+        p.variant |= kLaneCell;
+        d.n_chunks = round_up(d.n_cells * d.cpc, uint32_t(kProgThreads));
+      } else {
+        p.variant |= kWarpTile;
+      }
+    }
     if (!strat) {  // cells use a per-tile shift computed on the device
       double mid[MCB_MAX_DIM];
       for (uint32_t j = 0; j < f.dim; ++j) mid[j] = f.low[j] + 0.5 * (f.high[j] - f.low[j]);
@@ -524,7 +531,7 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     const size_t i = order[r];
     FnDesc d = prep[i].d;
     const int fam = int(fns[i].family), dim = int(fns[i].dim), var = prep[i].variant;
-    tile = round_up<uint64_t>(tile, mcb::detail::tiles_per_cta(var));
+    tile = round_up<uint64_t>(tile, mcb::detail::tile_align(var, fam == MCB_FAMILY_PROGRAM));
     d.tile_base = tile;
     d.out_slot = i;
     const uint64_t nt = uint64_t(d.n_chunks) * trials;
@@ -585,13 +592,10 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
 // look-ups, and with `compile` (plans, which are relaunched) parallel
 // compiles of the missing ones before the first launch.
 void prepare_programs(const HostPlan& hp, bool compile) {
-  using mcb::detail::kStrat;
-  using mcb::detail::kUnitDomain;
-  using mcb::detail::kWarpTile;
   std::vector<std::pair<const mcb::prog::Program*, int>> kernels;
   for (const auto& g : hp.groups) {
     if (!g.prog) continue;
-    const int km = (g.variant & kWarpTile) ? 3 : (g.variant & kStrat) ? 2 : (g.variant & kUnitDomain) ? 1 : 0;
+    const int km = mcb::detail::program_kernel_mode(g.variant);
     const auto k = std::make_pair(g.prog, km);
     if (std::find(kernels.begin(), kernels.end(), k) == kernels.end()) kernels.push_back(k);
   }

@@ -44,7 +44,8 @@ std::string last_error();
 
 // Launch the specialised kernel of `p` in kernel mode `mode` (0 direct, 1
 // direct on the unit cube, 2 cells CTA-per-tile, 3 small cells
-// warp-per-tile) over `ctas` CTAs of 128 threads starting at tile `tile0`;
+// warp-per-tile, 4 small cells of a large grid thread-per-cell) over `ctas`
+// CTAs of 128 threads starting at tile `tile0`;
 // `samples` (the launch's work) decides whether the automatic mode compiles
 // an uncached program.  Returns false (nothing launched) when the caller
 // should run the interpreter.
@@ -57,7 +58,7 @@ bool launch(const prog::Program& p, int mode, uint32_t ctas, uint64_t samples, c
 // missing ones in parallel.
 void prepare(const std::vector<std::pair<const prog::Program*, int>>& kernels, bool compile);
 
-// NVRTC-compile `p`'s four kernel modes (or find them in the disk cache)
+// NVRTC-compile `p`'s five kernel modes (or find them in the disk cache)
 // without a device: warms the on-disk cache ahead of time and checks the
 // generated code.
 bool compile_only(const prog::Program& p, std::string* err);

@@ -15,7 +15,8 @@
 //
 // Modes (the interpreter's variants): 0 direct, 1 direct on [0,1]^d,
 // 2 cell-structured (stratified / tree round, CTA per tile), 3 small cells
-// (warp per tile, kTileAlign-aligned tile groups).
+// (warp per tile, kTileAlign-aligned tile groups), 4 small cells of a large
+// grid (thread per cell, kProgThreads-aligned).
 #pragma once
 
 #include "mcb_device.cuh"
@@ -225,6 +226,44 @@ __device__ __forceinline__ void tile_warp(const FnDesc* __restrict__ fns, const 
   }
 }
 
+// Mode 4: small cells of a large grid, one thread per cell (k_program_lane).
+template <class P, int D>
+__device__ __forceinline__ void tile_lane(const FnDesc* __restrict__ fns, const uint32_t* __restrict__ tile_fn,
+                                          uint64_t tile0, TilePartial* __restrict__ part) {
+  const uint64_t group = tile0 + uint64_t(blockIdx.x) * T;
+  const uint32_t fi = __ldg(tile_fn + group);
+  FnDesc f = fns[fi];
+  const uint64_t tile = group + threadIdx.x;
+  const uint32_t rem = uint32_t(tile - f.tile_base);
+  const uint32_t trial = rem / f.n_chunks;
+  const uint32_t cell = rem - trial * f.n_chunks;
+  if (cell >= f.n_cells) return;  // padding thread of the aligned range
+  const uint32_t count = f.spc;
+  dev::cell_rect<D>(f, cell, 1.0);
+  const uint32_t pairs = (count + 1) >> 1;
+  const PhiloxPrefix Ph = dev::make_prefix(f.key0, f.key1, f.chunk_base + cell, f.trial_base + trial);
+  double params[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) params[i] = f.k[i];
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t nbad = 0;
+  {  // pair 0: its first sample is the cell's shift
+    double x0[D], x1[D];
+    gen_points<D, false>(f, Ph, 0, x0, x1);
+    const double f0 = P::eval(x0, params), f1 = P::eval(x1, params);
+    f.shift = finite64(f0) ? f0 : 0.0;
+    add_pair(f, 0, count, f0, f1, s1, s2, nbad);
+  }
+  accumulate<P, D, false>(f, Ph, params, 1, 1, pairs, count, s1, s2, nbad);
+  TilePartial p;
+  p.s1 = s1;
+  p.s2 = s2;
+  p.shift = f.shift;
+  p.n_nonfinite = nbad;
+  p.n_finite = count - nbad;
+  part[tile] = p;
+}
+
 }  // namespace jit
 }  // namespace mcb
 
@@ -233,12 +272,14 @@ __device__ __forceinline__ void tile_warp(const FnDesc* __restrict__ fns, const 
 // launch needs is compiled.
 template <int MODE>
 struct JitBounds {
-  static constexpr int min_blocks = MODE == 3 ? MCB_JIT_WARP_MIN_BLOCKS : 1;
+  static constexpr int min_blocks = MODE >= 3 ? MCB_JIT_WARP_MIN_BLOCKS : 1;
 };
 #define MCB_JIT_KERNEL(NAME, PROG, D, MODE)                                                         \
   extern "C" __global__ void __launch_bounds__(MCB_JIT_THREADS, JitBounds<MODE>::min_blocks)        \
       NAME(const mcb::dev::FnDesc* f, const uint32_t* t, uint64_t t0, mcb::dev::TilePartial* p) {   \
-    if constexpr (MODE == 3)                                                                        \
+    if constexpr (MODE == 4)                                                                        \
+      mcb::jit::tile_lane<PROG, D>(f, t, t0, p);                                                    \
+    else if constexpr (MODE == 3)                                                                   \
       mcb::jit::tile_warp<PROG, D>(f, t, t0, p);                                                    \
     else                                                                                            \
       mcb::jit::tile_cta<PROG, D, MODE>(f, t, t0, p);                                               \

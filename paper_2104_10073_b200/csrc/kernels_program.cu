@@ -321,6 +321,58 @@ __global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ f
   }
 }
 
+// Small cells of a large grid (kStrat | kLaneCell): the CTA covers
+// kProgThreads consecutive cells of one (integrand, trial) (ranges padded /
+// aligned to kProgThreads by the host), one THREAD per cell (one chunk per
+// cell): sample 0 is the cell's shift, the pairs in ascending order, the
+// cell's TilePartial written by its thread — no reduction.
+template <int D, int V>
+__global__ void __launch_bounds__(T) k_program_lane(const FnDesc* __restrict__ fns,
+                                                    const uint32_t* __restrict__ tile_fn, uint64_t tile0,
+                                                    TilePartial* __restrict__ part,
+                                                    const uint32_t* __restrict__ code,
+                                                    const double* __restrict__ consts, uint32_t slots) {
+  static_assert((V & kStrat) && (V & kLaneCell) && !(V & kWarpTile), "cell-per-lane variant");
+  const uint64_t group = tile0 + uint64_t(blockIdx.x) * T;
+  const uint32_t fi = __ldg(tile_fn + group);
+  FnDesc f = fns[fi];
+  __shared__ double params[prog::kMaxParams];
+  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  const uint64_t tile = group + threadIdx.x;
+  const uint32_t rem = uint32_t(tile - f.tile_base);
+  const uint32_t trial = rem / f.n_chunks;
+  const uint32_t cell = rem - trial * f.n_chunks;
+  if (cell >= f.n_cells) return;  // padding thread of the aligned range
+  const uint32_t count = f.spc;
+  dev::cell_rect<D>(f, cell, 1.0);
+  const uint32_t pairs = (count + 1) >> 1;
+  const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + cell, f.trial_base + trial);
+  double s1 = 0.0, s2 = 0.0;
+  uint32_t nbad = 0;
+  for (uint32_t q = 0; q < pairs; ++q) {
+    gen_points<D, false>(f, P, q, m.X);
+    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+    const double f0 = m.S[threadIdx.x], f1 = m.S[T + threadIdx.x];
+    if (q == 0) f.shift = finite64(f0) ? f0 : 0.0;
+    const bool has1 = 2 * q + 1 < count;
+    const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
+    nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+    const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
+    const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
+    s1 = __dadd_rn(s1, g0);
+    s2 = fma(g0, g0, s2);
+    s1 = __dadd_rn(s1, g1);
+    s2 = fma(g1, g1, s2);
+  }
+  TilePartial p;
+  p.s1 = s1;
+  p.s2 = s2;
+  p.shift = f.shift;
+  p.n_nonfinite = nbad;
+  p.n_finite = count - nbad;
+  part[tile] = p;
+}
+
 // Per-sample values of pairs [first_pair, first_pair + n_pairs) of one chunk
 // (test hook): exactly the gen_points/interp_pair of k_program.
 template <int D, int V>
@@ -356,13 +408,14 @@ struct ProgEntry {
 };
 
 struct ProgTable {
-  ProgEntry e[MCB_MAX_DIM + 1][4];  // general domain, unit domain, cells, small cells
+  ProgEntry e[MCB_MAX_DIM + 1][5];  // by program_kernel_mode: general / unit domain, cells, small cells (warp, lane)
   template <int D>
   void put() {
     e[D][0] = {k_program<D, kSafe>, k_program_eval<D, kSafe>};
     e[D][1] = {k_program<D, kSafe | kUnitDomain>, k_program_eval<D, kSafe | kUnitDomain>};
     e[D][2] = {k_program<D, kSafe | kStrat>, k_program_eval<D, kSafe>};
     e[D][3] = {k_program_warp<D, kSafe | kStrat | kWarpTile>, k_program_eval<D, kSafe>};
+    e[D][4] = {k_program_lane<D, kSafe | kStrat | kLaneCell>, k_program_eval<D, kSafe>};
   }
   ProgTable() {
     put<1>();
@@ -393,7 +446,7 @@ static cudaError_t ensure_smem_optin() {
   if (done.count(dev)) return cudaSuccess;
   const ProgTable& t = prog_table();
   for (int d = 1; d <= int(MCB_MAX_DIM); ++d)
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 5; ++v) {
       const int smem = int(program_smem_bytes(prog::kMaxDepth, d));
       if ((e = cudaFuncSetAttribute(t.e[d][v].run, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem)) != cudaSuccess)
@@ -408,7 +461,7 @@ static cudaError_t ensure_smem_optin() {
 
 static const ProgEntry* prog_entry(int dim, int variant) {
   if (dim < 1 || dim > int(MCB_MAX_DIM)) return nullptr;
-  return &prog_table().e[dim][(variant & kWarpTile) ? 3 : (variant & kStrat) ? 2 : (variant & kUnitDomain) ? 1 : 0];
+  return &prog_table().e[dim][program_kernel_mode(variant)];
 }
 
 cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const uint32_t* tile_fn,
@@ -416,11 +469,11 @@ cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const 
                                  cudaStream_t s) {
   const ProgEntry* e = prog_entry(g.dim, g.variant);
   if (!e) return cudaErrorInvalidValue;
-  const uint64_t per_cta = (g.variant & kWarpTile) ? uint64_t(T / 32) : 1u;  // tiles per CTA
+  const uint64_t per_cta = tiles_per_cta(g.variant, true);
   const uint64_t n_ctas = g.n_tiles / per_cta;
   const uint64_t kMaxGrid = 0x7FFFFFF8ull;
   if (g.prog && n_ctas <= kMaxGrid) {  // runtime-specialised kernel of this program (jit.hpp)
-    const int mode = (g.variant & kWarpTile) ? 3 : (g.variant & kStrat) ? 2 : (g.variant & kUnitDomain) ? 1 : 0;
+    const int mode = program_kernel_mode(g.variant);
     cudaError_t err = cudaSuccess;
     if (jit::launch(*g.prog, mode, uint32_t(n_ctas), g.n_tiles * MCB_CHUNK_SIZE, fns, tile_fn, g.tile0, part, s,
                     &err))

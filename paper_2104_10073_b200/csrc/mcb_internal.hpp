@@ -58,9 +58,26 @@ constexpr uint32_t kWarpTileMaxSpc = 8192;
 constexpr uint32_t kLaneAlign = 32;
 constexpr uint32_t kLaneCellMinCells = 256;
 
-// Tiles per CTA and tile-range alignment of a variant's kernel.
-constexpr uint32_t tiles_per_cta(int variant) {
-  return (variant & kLaneCell) ? kLaneAlign : (variant & kWarpTile) ? kTileAlign : 1u;
+// DSL programs: a lane per cell on grids of at least this many cells
+// (one CTA = kProgThreads cells, so ranges are padded to kProgThreads).
+constexpr uint32_t kProgLaneMinCells = 1024;
+
+// Tiles per CTA of a variant's kernel (family kernels / the DSL programs'
+// interpreter and specialised kernels, kProgThreads per CTA).
+constexpr uint32_t tiles_per_cta(int variant, bool program = false) {
+  return program ? ((variant & kLaneCell) ? uint32_t(kProgThreads) : (variant & kWarpTile) ? uint32_t(kProgThreads / 32) : 1u)
+                 : ((variant & kLaneCell) ? kLaneAlign : (variant & kWarpTile) ? kTileAlign : 1u);
+}
+// Alignment of a variant's tile ranges (per (integrand, trial) and per
+// descriptor): the CTA's tiles, and kTileAlign for any warp-per-tile group.
+constexpr uint32_t tile_align(int variant, bool program = false) {
+  return (variant & kWarpTile) ? kTileAlign : tiles_per_cta(variant, program);
+}
+// Kernel mode of a DSL program group (jit_kernels.cuh, kernels_program.cu):
+// 0 direct, 1 direct on [0,1]^d, 2 cells (CTA per tile), 3 small cells (warp
+// per tile), 4 small cells of a large grid (lane per cell).
+constexpr int program_kernel_mode(int variant) {
+  return (variant & kLaneCell) ? 4 : (variant & kWarpTile) ? 3 : (variant & kStrat) ? 2 : (variant & kUnitDomain) ? 1 : 0;
 }
 static_assert(kThreads / 32 == int(kTileAlign), "family CTA = kTileAlign warps");
 static_assert(kTileAlign % (kProgThreads / 32) == 0, "interpreter CTAs tile the aligned groups");

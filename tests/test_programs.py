@@ -281,8 +281,9 @@ def test_cos_plus_sin_fusion(gpu):
 @pytest.mark.gpu
 def test_jit_bit_identical_to_interpreter(gpu, progs):
     """Runtime-specialised programs (NVRTC, csrc/jit.cpp) against the bytecode
-    interpreter: every per-trial McEstimate byte-identical, in all four modes
-    (direct, unit cube, cells CTA-per-tile, small cells warp-per-tile), for
+    interpreter: every per-trial McEstimate byte-identical, in all five modes
+    (direct, unit cube, cells CTA-per-tile, small cells warp-per-tile, small
+    cells of a large grid thread-per-cell), for
     the golden programs incl. non-finite patterns and the random ones."""
     assert gpu.program_jit(2) == 2, gpu.program_jit_error()  # always: every launch specialised
     keep, fns = [], []
@@ -296,7 +297,8 @@ def test_jit_bit_identical_to_interpreter(gpu, progs):
     fns.append(unit.integrand(n_samples=100_000, index=len(fns)))          # mode 1
     cells = unit.integrand(low=[-1, 0, 0], high=[1, 2, 1], n_samples=300_000, index=len(fns) + 1)
     fns.append(gpu.stratify(cells, cells_per_dim=2))                         # mode 2 (75 000 / cell)
-    fns.append(gpu.stratify(unit.integrand(n_samples=200_000, index=len(fns) + 2)))  # mode 3
+    fns.append(gpu.stratify(unit.integrand(n_samples=200_000, index=len(fns) + 2), cells_per_dim=8))  # mode 3
+    fns.append(gpu.stratify(unit.integrand(n_samples=200_000, index=len(fns) + 2)))  # mode 4: 16^3 cells
     fns.append(gpu.tree(unit.integrand(n_samples=80_000, index=len(fns) + 3), samples_per_cell=500))
     n0 = gpu.program_jit_compiles()
     a = gpu.run_direct(fns, 99, 2)
@@ -322,7 +324,7 @@ def test_jit_code_compiles_for_every_golden_program(mcb, progs, tmp_path, monkey
         p = mcb.Program("(" + src + ")" + salt, dim, names)
         p.jit_build()
         assert mcb.program_jit_error() == "", (src, mcb.program_jit_error())
-    assert len(list(tmp_path.iterdir())) >= 4 * len(srcs)  # four kernel modes each, cached
+    assert len(list(tmp_path.iterdir())) >= 5 * len(srcs)  # five kernel modes each, cached
 
 
 @pytest.mark.gpu
@@ -355,13 +357,13 @@ def test_jit_automatic_mode(gpu, tmp_path, monkeypatch):
     n0 = gpu.program_jit_compiles()
     first = gpu.run_direct([f], 17, 3)  # interpreter: not cached, too small to compile
     assert gpu.program_jit_compiles() == n0
-    p.jit_build()  # all four kernel modes
-    assert gpu.program_jit_compiles() == n0 + 4
+    p.jit_build()  # all five kernel modes
+    assert gpu.program_jit_compiles() == n0 + 5
     later = gpu.run_direct([f], 17, 3)  # specialised (in memory now)
     assert first.tobytes() == later.tobytes()
     q = gpu.Program("exp(-b*(x1-0.25)^2) * (1 + 0.5*sin(9*x2)) + x2", 2, ["b"])
     plan = gpu.Plan([q.integrand({"b": 7.5}, n_samples=300_000, index=4)], 17, 3)  # plans compile their mode
-    assert gpu.program_jit_compiles() == n0 + 5
+    assert gpu.program_jit_compiles() == n0 + 6
     plan.close()
 
 

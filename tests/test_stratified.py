@@ -136,6 +136,28 @@ def test_stratified_program_and_dead_cells(gpu, oracle):
         var += se * se
     assert abs(got["value"] - value) <= 1e-12 * abs(value)
     assert abs(got["std_error"] - var ** 0.5) <= 1e-9 * var ** 0.5
+    # 32x32 cells of 8 samples: the thread-per-cell kernels (interpreter and
+    # specialised), against the same oracle
+    k, spc = 32, 8
+    for jit in (0, 2):
+        gpu.program_jit(jit)
+        try:
+            g = gpu.stratify(prog.integrand({"a": 20.0}, n_samples=k * k * spc, index=6), cells_per_dim=k)
+            got = gpu.run_direct([g], 123, 1)[0, 0]
+        finally:
+            gpu.program_jit(1)
+        value, var = 0.0, 0.0
+        for c in range(k * k):
+            lo, hi = (ctypes.c_double * 8)(), (ctypes.c_double * 8)()
+            oracle.orc_grid_cell(ctypes.byref(g), k, c, lo, hi)
+            pts = _oracle.sample_uniform([lo[0], lo[1]], [hi[0], hi[1]], 123, 6, 0, c, 0, spc)
+            vol = (hi[0] - lo[0]) * (hi[1] - lo[1])
+            v, se, _, _ = dsl.welford_direct_mc([[ora(r) for r in pts]], vol)
+            value += v
+            var += se * se
+        assert int(got["n_samples"]) == k * k * spc and int(got["n_cells"]) == k * k
+        assert abs(got["value"] - value) <= 1e-12 * abs(value), jit
+        assert abs(got["std_error"] - var ** 0.5) <= 1e-9 * var ** 0.5, jit
 
 
 @pytest.mark.gpu
