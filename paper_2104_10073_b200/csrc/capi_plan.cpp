@@ -552,8 +552,13 @@ mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed
     }
     const mcb::prog::Program* gp = fam == MCB_FAMILY_PROGRAM ? &fns[i].program->p : nullptr;
     if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
-        hp.groups.back().variant != var || hp.groups.back().prog != gp)
+        hp.groups.back().variant != var || hp.groups.back().prog != gp) {
       hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0, gp});
+      hp.groups.back().tile_samples = 0;
+    }
+    const uint64_t per_tile = d.strat_k > 0 ? d.spc : fns[i].n_samples;
+    hp.groups.back().tile_samples =
+        std::max(hp.groups.back().tile_samples, uint32_t(std::min<uint64_t>(per_tile, MCB_CHUNK_SIZE)));
     hp.groups.back().n_tiles += nt;
     hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
     tile += nt;

@@ -120,8 +120,11 @@ mcb_status run_cell_shard(const std::vector<const mcb::tree::CellBatch*>& batche
     }
     const mcb::prog::Program* gp = fam == MCB_FAMILY_PROGRAM ? &b.fn->program->p : nullptr;
     if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
-        hp.groups.back().variant != var || hp.groups.back().prog != gp)
+        hp.groups.back().variant != var || hp.groups.back().prog != gp) {
       hp.groups.push_back(GroupLaunch{fam, dim, var, tile, 0, 0, gp});
+      hp.groups.back().tile_samples = 0;
+    }
+    hp.groups.back().tile_samples = std::max(hp.groups.back().tile_samples, std::min<uint32_t>(b.spc, MCB_CHUNK_SIZE));
     hp.groups.back().n_tiles += d.n_chunks;
     hp.groups.back().slots = std::max(hp.groups.back().slots, slots);
     tile += d.n_chunks;
@@ -266,8 +269,11 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     const int fam = int(f.family), dim = int(f.dim), var = h.prep.variant;
     const mcb::prog::Program* gp = fam == MCB_FAMILY_PROGRAM ? &f.program->p : nullptr;
     if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
-        hp.groups.back().variant != var || hp.groups.back().prog != gp)
+        hp.groups.back().variant != var || hp.groups.back().prog != gp) {
       hp.groups.push_back(GroupLaunch{fam, dim, var, 0, 0, 0, gp});
+      hp.groups.back().tile_samples = 0;
+    }
+    hp.groups.back().tile_samples = std::max(hp.groups.back().tile_samples, std::min<uint32_t>(h.spc, MCB_CHUNK_SIZE));
     FnDesc d = h.prep.d;
     d.strat_k = 0;
     d.spc = h.spc;

@@ -475,7 +475,7 @@ cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const 
   if (g.prog && n_ctas <= kMaxGrid) {  // runtime-specialised kernel of this program (jit.hpp)
     const int mode = program_kernel_mode(g.variant);
     cudaError_t err = cudaSuccess;
-    if (jit::launch(*g.prog, mode, uint32_t(n_ctas), g.n_tiles * MCB_CHUNK_SIZE, fns, tile_fn, g.tile0, part, s,
+    if (jit::launch(*g.prog, mode, uint32_t(n_ctas), g.n_tiles * g.tile_samples, fns, tile_fn, g.tile0, part, s,
                     &err))
       return err;
   }

@@ -89,6 +89,7 @@ struct GroupLaunch {
   uint64_t tile0, n_tiles;
   uint32_t slots = 0;  // PROGRAM family: max stack depth of the group's programs
   const prog::Program* prog = nullptr;  // PROGRAM family: the group's one program (runtime-specialised)
+  uint32_t tile_samples = MCB_CHUNK_SIZE;  // most samples one tile of the group draws (JIT policy)
 };
 
 bool variant_supported(int family, int dim, int variant);
