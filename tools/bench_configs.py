@@ -58,7 +58,9 @@ def main():
         "c5": lambda: w.c5(n_fns=args.c5_fns),
     }
     stream = torch.cuda.current_stream()
-    mcb.program_jit(2)  # program configs: specialised kernels compiled before the first launch
+    # program configs: specialised kernels compiled before the first launch
+    # (MCB_PROGRAM_JIT=0 in the environment measures the bytecode interpreter)
+    mcb.program_jit(0 if os.environ.get("MCB_PROGRAM_JIT") == "0" else 2)
     peak = mcb.probe_philox_peak(0, 50.0)
     out = {"philox_peak_blocks_per_s": peak}
     for name in args.configs.split(","):
