@@ -158,6 +158,30 @@ def test_stratified_program_and_dead_cells(gpu, oracle):
         assert int(got["n_samples"]) == k * k * spc and int(got["n_cells"]) == k * k
         assert abs(got["value"] - value) <= 1e-12 * abs(value), jit
         assert abs(got["std_error"] - var ** 0.5) <= 1e-9 * var ** 0.5, jit
+    # thread-per-cell with non-finite samples: log(x1 - 0.3) on [0, 1] in 2048 cells — the
+    # cells below 0.3 have no finite sample, so the trial fails on the first dead cell (0),
+    # as the reference does; log(x1 + 1e-3) (all finite) against the oracle cell by cell
+    for jit in (0, 2):
+        gpu.program_jit(jit)
+        try:
+            q = gpu.Program("log(x1 - c)", 1, ["c"])
+            dead = gpu.stratify(q.integrand({"c": 0.3}, n_samples=2048 * 4, index=7), cells_per_dim=2048)
+            out = gpu.run_direct([dead], 5, 2)
+            assert (out["status"] == gpu.TRIAL_DEAD_CELL).all() and (out["detail"] == 0).all(), jit
+            live = gpu.stratify(q.integrand({"c": -1e-3}, n_samples=2048 * 4, index=8), cells_per_dim=2048)
+            got = gpu.run_direct([live], 5, 1)[0, 0]
+        finally:
+            gpu.program_jit(1)
+        assert int(got["status"]) == 0 and int(got["n_cells"]) == 2048
+        ora = dsl.Program("log(x1 - c)", 1, {"c": -1e-3})
+        value = 0.0
+        for c in range(2048):
+            lo, hi = (ctypes.c_double * 8)(), (ctypes.c_double * 8)()
+            oracle.orc_grid_cell(ctypes.byref(live), 2048, c, lo, hi)
+            pts = _oracle.sample_uniform([lo[0]], [hi[0]], 5, 8, 0, c, 0, 4)
+            v, _, _, _ = dsl.welford_direct_mc([[ora(r) for r in pts]], hi[0] - lo[0])
+            value += v
+        assert abs(got["value"] - value) <= 1e-12 * abs(value), jit
 
 
 @pytest.mark.gpu
