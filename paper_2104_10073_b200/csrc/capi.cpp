@@ -441,17 +441,16 @@ mcb_status mcb_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
   if (fn->n_samples < 2) return fail(MCB_ERR_INVALID_ARGUMENT, "n_samples must be >= 2");
   if (chunk_base + chunk_count(fn->n_samples) - 1 > 0xFFFFFFFFull)
     return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
-  // One (integrand, trial) unit: a 1-trial plan whose key base is
-  // {seed, integrand_index, trial, chunk_base}.
+  // One (integrand, trial) unit whose key base is {seed, integrand_index,
+  // trial, chunk_base}, on the device's persistent context (no per-call
+  // allocations: a call costs H2D + kernels + D2H).
   mcb_integrand f = *fn;  // direct_mc ignores the spec's method
   f.method = MCB_METHOD_DIRECT;
-  mcb_plan* plan = nullptr;
-  mcb_status st = plan_create_impl(&f, 1, seed, 1, device, uint32_t(chunk_base), trial, &plan);
+  mcb_status st = validate_for_run(&f, 1, 1);
   if (st != MCB_OK) return st;
-  st = plan_launch_impl(plan, nullptr);
-  if (st == MCB_OK) st = plan_download_impl(plan, out, nullptr);
-  mcb_plan_destroy(plan);
-  return st;
+  if ((st = check_device(device)) != MCB_OK) return st;
+  const uint32_t cb = uint32_t(chunk_base), tb = trial;
+  return run_shard(&f, 1, seed, 1, device, out, &cb, &tb);
 }
 
 mcb_status mcb_debug_points(uint64_t seed, uint32_t integrand_index, uint32_t trial, uint64_t chunk,
