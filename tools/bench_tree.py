@@ -6,7 +6,7 @@ stop below their budget when no leaf stands out — and the samples the kernels
 actually draw (split parents included), and the reference's own CPU run_batch on a
 bounded sample of the same trees (oracle/_ref, all host threads) when present.
 
-  python tools/bench_tree.py [--fns 200] [--trials 10] [--budget 1000000] [--ref-fns 8]
+  python tools/bench_tree.py [--fns 200] [--trials 10] [--budget 1000000] [--ref-fns 40]
 """
 import argparse
 import json
@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--budget", type=int, default=1_000_000)
     ap.add_argument("--spc", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--ref-fns", type=int, default=8)
+    ap.add_argument("--ref-fns", type=int, default=40)
     ap.add_argument("--integrand", choices=["harmonic", "peak"], default="harmonic",
                     help="harmonic: Fig.1 family (4-D); peak: the C5 gaussian peak DSL program (2-D)")
     args = ap.parse_args()
