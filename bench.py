@@ -70,6 +70,7 @@ def dist_env():
 class Dist:
     def __init__(self, world, rank, backend):
         self.world, self.rank = world, rank
+        self.backend = backend
         self.pg = None
         if world > 1:
             import torch.distributed as dist
@@ -85,7 +86,7 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        t = torch.tensor([x], dtype=torch.float64, device=device if self.backend == "nccl" else None)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -224,8 +225,10 @@ def run_mcb_arm(args, dist, local):
     import paper_2104_10073_b200 as mcb
     from paper_2104_10073_b200 import workloads
 
-    torch.cuda.set_device(local)
-    dev = local
+    # MCB_BENCH_SHARE_GPU=1 (test hook, gloo): ranks share the visible GPUs so the N > 1 code
+    # path can run on a one-GPU box; the ranks then compete for one GPU and the numbers mean nothing
+    dev = local % torch.cuda.device_count() if os.environ.get("MCB_BENCH_SHARE_GPU") == "1" else local
+    torch.cuda.set_device(dev)
     if args.scaling == "strong":  # one C2 set, rank r integrates its contiguous slice
         fns, seed, trials = workloads.c2(samples=args.samples, n_count=args.n_fns)
         lo, hi = strong_slice(args.n_fns, dist.rank, dist.world)
@@ -384,7 +387,7 @@ def main():
             print(json.dumps(line), flush=True)
         return
     import torch
-    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    backend = "nccl" if torch.cuda.is_available() and os.environ.get("MCB_BENCH_SHARE_GPU") != "1" else "gloo"
     dist = Dist(world, rank, backend)
     line = run_mcb_arm(args, dist, local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -1,0 +1,43 @@
+"""bench.py's N > 1 path (torchrun, one process per rank, barrier + max over
+ranks, rank 0 prints one JSON line) run on a one-GPU box: MCB_BENCH_SHARE_GPU=1
+puts both ranks on the visible GPU over gloo.  The ranks compete for one GPU,
+so only the contract is checked here, never the numbers."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun(extra):
+    env = dict(os.environ, MCB_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--samples", "100000", "--n-fns", "200",
+           "--no-clocks", *extra]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]  # rank 0 only
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_two_ranks(scaling):
+    line = _torchrun(["--scaling", scaling])
+    assert line["n_gpus"] == 2 and line["scaling"] == scaling and line["steps"] == 3
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    # value = samples of all ranks per step / the slowest rank's step time
+    per_step = (2 * 200 if scaling == "weak" else 200) * 100_000 * 10
+    assert line["value"] * line["ms_per_step"] / 1e3 == pytest.approx(per_step, rel=1e-9)
