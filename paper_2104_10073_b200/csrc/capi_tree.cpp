@@ -207,29 +207,38 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
   const size_t T = tasks.size();
   if (T == 0) return MCB_OK;
   // ---- host: configs, first-pass grids, descriptors, launch groups ----
-  struct HostTree {
+  struct HostTree {  // per distinct integrand: its trials share config, grid and descriptor
     mcb::tree::Config cfg;
     uint32_t k = 0, spc = 0, cpc = 0, fail = 0;
     uint64_t n0 = 0, cap = 0;
     Prepared prep;
   };
-  std::vector<HostTree> ht(T);
-  std::map<const mcb_integrand*, size_t> first_of;  // trials of one integrand share grid and descriptor
+  struct TrialOf {  // per tree: its integrand's HostTree and its own first-pass outcome
+    size_t base;
+    uint32_t fail;
+    uint64_t n0, cap;
+  };
+  std::vector<HostTree> ht;
+  std::vector<TrialOf> tr(T);
+  std::map<const mcb_integrand*, size_t> first_of;
   for (size_t i = 0; i < T; ++i) {
     const mcb_integrand& f = *tasks[i]->fn;
-    HostTree& h = ht[i];
-    auto seen = first_of.find(tasks[i]->fn);
-    if (seen != first_of.end()) {
-      h = ht[seen->second];
-      h.prep.d.trial_base = tasks[i]->trial;
-      if (!h.fail && tasks[i]->chunk_base + h.n0 * h.cpc - 1 > 0xFFFFFFFFull) {
-        h.fail = MCB_TRIAL_CHUNK_RANGE;
-        h.n0 = 0;
-        h.cap = tree_leaf_bound(0, h.spc, h.cfg) + 1;
-      }
+    // an integrand's trials are usually adjacent: skip the map look-up for them
+    size_t seen_base = i > 0 && tasks[i - 1]->fn == tasks[i]->fn ? tr[i - 1].base : SIZE_MAX;
+    if (seen_base == SIZE_MAX) {
+      auto seen = first_of.find(tasks[i]->fn);
+      if (seen != first_of.end()) seen_base = seen->second;
+    }
+    if (seen_base != SIZE_MAX) {
+      const HostTree& h = ht[seen_base];
+      tr[i] = TrialOf{seen_base, h.fail, h.n0, h.cap};
+      if (!h.fail && tasks[i]->chunk_base + h.n0 * h.cpc - 1 > 0xFFFFFFFFull)
+        tr[i] = TrialOf{seen_base, MCB_TRIAL_CHUNK_RANGE, 0, tree_leaf_bound(0, h.spc, h.cfg) + 1};
       continue;
     }
-    first_of.emplace(tasks[i]->fn, i);
+    first_of.emplace(tasks[i]->fn, ht.size());
+    ht.emplace_back();
+    HostTree& h = ht.back();
     h.cfg = mcb::tree::config_of(f);
     h.spc = std::max<uint32_t>(h.cfg.samples_per_cell, 2);
     h.cpc = uint32_t(chunk_count(h.spc));
@@ -246,26 +255,32 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     if (h.cap > 0xFFFFFFFFull) return fail(MCB_ERR_INVALID_ARGUMENT, "tree budget too large for one device run");
     h.prep = prepare(f, seed, 0, tasks[i]->trial, true);
     if (h.spc <= kWarpTileMaxSpc) h.prep.variant |= kWarpTile;
+    tr[i] = TrialOf{ht.size() - 1, h.fail, h.n0, h.cap};
   }
   const auto t_cfg = tclk::now();
   std::vector<size_t> order(T);  // launch groups: (family, dim, variant, program)
   std::iota(order.begin(), order.end(), size_t(0));
-  auto key = [&](size_t i) {
+  using Key = std::tuple<uint32_t, uint32_t, int, uintptr_t>;
+  std::vector<Key> keys(T);
+  for (size_t i = 0; i < T; ++i) {
     const mcb_integrand& f = *tasks[i]->fn;
-    return std::make_tuple(f.family, f.dim, ht[i].prep.variant,
-                           f.family == MCB_FAMILY_PROGRAM ? reinterpret_cast<uintptr_t>(f.program) : uintptr_t(0));
-  };
-  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return key(a) < key(b); });
+    keys[i] = Key(f.family, f.dim, ht[tr[i].base].prep.variant,
+                  f.family == MCB_FAMILY_PROGRAM ? reinterpret_cast<uintptr_t>(f.program) : uintptr_t(0));
+  }
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return keys[a] < keys[b]; });
   HostPlan hp;
   std::vector<TreeConst> tc(T);
   std::vector<TreeState> tst(T);
   std::map<const mcb_program*, std::pair<uint32_t, uint32_t>> prog_at;
+  const mcb_program* last_prog = nullptr;
+  std::pair<uint32_t, uint32_t> last_at{0, 0};
   uint64_t leaves = 0, rect_doubles = 0, max_tiles = 0;
   hp.descs.resize(T);
   for (size_t r = 0; r < T; ++r) {
     const size_t i = order[r];
     const mcb_integrand& f = *tasks[i]->fn;
-    HostTree& h = ht[i];
+    const HostTree& h = ht[tr[i].base];
+    const TrialOf& t = tr[i];
     const int fam = int(f.family), dim = int(f.dim), var = h.prep.variant;
     const mcb::prog::Program* gp = fam == MCB_FAMILY_PROGRAM ? &f.program->p : nullptr;
     if (hp.groups.empty() || hp.groups.back().family != fam || hp.groups.back().dim != dim ||
@@ -274,31 +289,36 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
       hp.groups.back().tile_samples = 0;
     }
     hp.groups.back().tile_samples = std::max(hp.groups.back().tile_samples, std::min<uint32_t>(h.spc, MCB_CHUNK_SIZE));
-    FnDesc d = h.prep.d;
+    FnDesc& d = hp.descs[r];
+    d = h.prep.d;
+    d.trial_base = tasks[i]->trial;
     d.strat_k = 0;
     d.spc = h.spc;
     d.cpc = h.cpc;
     d.out_slot = r;
     if (fam == MCB_FAMILY_PROGRAM) {
-      auto it = prog_at.find(f.program);
-      if (it == prog_at.end()) {
-        it = prog_at.emplace(f.program, std::make_pair(uint32_t(hp.code.size()), uint32_t(hp.consts.size()))).first;
-        hp.code.insert(hp.code.end(), f.program->words.begin(), f.program->words.end());
-        hp.consts.insert(hp.consts.end(), f.program->p.consts.begin(), f.program->p.consts.end());
+      if (f.program != last_prog) {  // trees of one program are adjacent after the sort
+        auto it = prog_at.find(f.program);
+        if (it == prog_at.end()) {
+          it = prog_at.emplace(f.program, std::make_pair(uint32_t(hp.code.size()), uint32_t(hp.consts.size()))).first;
+          hp.code.insert(hp.code.end(), f.program->words.begin(), f.program->words.end());
+          hp.consts.insert(hp.consts.end(), f.program->p.consts.begin(), f.program->p.consts.end());
+        }
+        last_prog = f.program;
+        last_at = it->second;
       }
-      d.prog_off = it->second.first;
+      d.prog_off = last_at.first;
       d.prog_len = uint32_t(f.program->p.code.size());
-      d.const_off = it->second.second;
+      d.const_off = last_at.second;
       d.n_consts = uint32_t(f.program->p.consts.size());
       hp.groups.back().slots = std::max(hp.groups.back().slots, f.program->p.depth);
     }
-    hp.descs[r] = d;
     TreeConst& c = tc[r];
     c.leaf_off = leaves;
     c.rect_off = rect_doubles;
     c.budget = h.cfg.total_budget;
     c.sigma = h.cfg.sigma_multiplier;
-    c.leaf_cap = uint32_t(h.cap);
+    c.leaf_cap = uint32_t(t.cap);
     c.dim = f.dim;
     c.spc = h.spc;
     c.cpc = h.cpc;
@@ -308,16 +328,16 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
     c.reserved = 0;
     TreeState& st = tst[r];
     std::memset(&st, 0, sizeof st);
-    st.fail = h.fail;
-    st.n_leaves = uint32_t(h.n0);
-    st.n_new = uint32_t(h.n0);
-    st.active = h.fail ? 0u : 1u;
+    st.fail = t.fail;
+    st.n_leaves = uint32_t(t.n0);
+    st.n_new = uint32_t(t.n0);
+    st.active = t.fail ? 0u : 1u;
     st.chunk0 = tasks[i]->chunk_base;
-    st.next_chunk = tasks[i]->chunk_base + h.n0 * h.cpc;
-    st.used = h.n0 * h.spc;
-    leaves += h.cap;
-    rect_doubles += h.cap * 2 * f.dim;
-    max_tiles += (h.cap * h.cpc + kTileAlign - 1) / kTileAlign * kTileAlign;
+    st.next_chunk = tasks[i]->chunk_base + t.n0 * h.cpc;
+    st.used = t.n0 * h.spc;
+    leaves += t.cap;
+    rect_doubles += t.cap * 2 * f.dim;
+    max_tiles += (t.cap * h.cpc + kTileAlign - 1) / kTileAlign * kTileAlign;
   }
   max_tiles += kTileAlign * hp.groups.size();
   if (hp.groups.size() > 256) return fail(MCB_ERR_INVALID_ARGUMENT, "too many distinct tree kernels in one run");
@@ -330,16 +350,23 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
   uint64_t packed_doubles = 0;
   std::map<const mcb_integrand*, uint64_t> grid_at;  // packed offset of an integrand's grid
   std::vector<size_t> grid_rows;                      // one tree per distinct grid
+  const mcb_integrand* last_fn = nullptr;
+  uint64_t last_off = 0;
   for (size_t r = 0; r < T; ++r) {
     tc[r].init_off = 0;
     if (tst[r].n_leaves == 0) continue;  // failed before the first pass
-    auto it = grid_at.find(tasks[order[r]]->fn);
-    if (it == grid_at.end()) {
-      it = grid_at.emplace(tasks[order[r]]->fn, packed_doubles).first;
-      packed_doubles += uint64_t(tst[r].n_leaves) * 2 * tc[r].dim;
-      grid_rows.push_back(r);
+    const mcb_integrand* fn = tasks[order[r]]->fn;
+    if (fn != last_fn) {  // trials of one integrand are adjacent after the (stable) sort
+      auto it = grid_at.find(fn);
+      if (it == grid_at.end()) {
+        it = grid_at.emplace(fn, packed_doubles).first;
+        packed_doubles += uint64_t(tst[r].n_leaves) * 2 * tc[r].dim;
+        grid_rows.push_back(r);
+      }
+      last_fn = fn;
+      last_off = it->second;
     }
-    tc[r].init_off = it->second;
+    tc[r].init_off = last_off;
   }
   const auto t_desc = tclk::now();
   DeviceCtx& c = device_ctx(device);
@@ -351,7 +378,7 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
   for (size_t r : grid_rows) {
     const size_t i = order[r];
     const mcb_integrand& f = *tasks[i]->fn;
-    const uint32_t k = ht[i].k, D = f.dim;
+    const uint32_t k = ht[tr[i].base].k, D = f.dim;
     for (uint64_t cell = 0; cell < tst[r].n_leaves; ++cell) {
       double* lo = c.h_rects + tc[r].init_off + 2 * D * cell;
       double* hi = lo + D;
