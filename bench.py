@@ -324,10 +324,29 @@ def run_mcb_arm(args, dist, local):
                              "time; peak = mcb_probe_philox_peak (Philox-only, same code, measured live); "
                              "traffic = dram__bytes_read+write of this k_direct launch from " + NCU_SUMMARY +
                              " (tile table + descriptors; the kernel is ALU-bound, SURVEY.md §8(d))",
-                     "hbm": hbm_roofline(ncu_traffic(), kernel_s / args.steps)},
+                     "hbm": hbm_roofline(ncu_traffic(), kernel_s / args.steps),
+                     "fused": fused_roofline(achieved, clk.summary())},
         "clocks": clk.summary(),
     }
     return line
+
+
+# Philox4x32-10 + the 14-op table harmonic on the shared IMAD.WIDE/FP64 pipe,
+# blocks per clock per SM (tools/micro/split_micro.cu "ph+trig WIDE x17",
+# profiles/r01_microbench.txt): the ceiling of this integrand, not of Philox alone.
+FUSED_BLOCKS_PER_CLK_SM = 1.306
+
+
+def fused_roofline(achieved_blocks_s, clocks):
+    """The same launch against the synthetic Philox + table-trig ceiling at the
+    SM clock sampled during the timed region (148 SMs)."""
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz")
+    if not mhz:
+        return None
+    peak = FUSED_BLOCKS_PER_CLK_SM * 148 * mhz * 1e6
+    return {"bound": "alu: Philox + 14-op harmonic, shared IMAD.WIDE/FP64 pipe", "achieved": achieved_blocks_s / 1e9,
+            "peak": peak / 1e9, "unit": "G Philox blocks/s", "frac": achieved_blocks_s / peak,
+            "peak_source": "tools/micro/split_micro.cu (1.306 blocks/clk/SM) x 148 SMs x sampled SM clock"}
 
 
 NCU_SUMMARY = "profiles/r01_bench_k_direct_ncu_summary.txt"
