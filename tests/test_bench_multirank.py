@@ -38,6 +38,15 @@ def test_bench_two_ranks(scaling):
     line = _torchrun(["--scaling", scaling])
     assert line["n_gpus"] == 2 and line["scaling"] == scaling and line["steps"] == 3
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    assert line["roofline"]["frac"] > 0 and "cpu_baseline" not in line  # the CPU leg is rank 0 at N = 1 only
     # value = samples of all ranks per step / the slowest rank's step time
     per_step = (2 * 200 if scaling == "weak" else 200) * 100_000 * 10
     assert line["value"] * line["ms_per_step"] / 1e3 == pytest.approx(per_step, rel=1e-9)
+
+
+def test_fused_roofline_arithmetic():
+    import bench
+    r = bench.fused_roofline(3.0e11, {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0})
+    assert r["peak"] == pytest.approx(1.306 * 148 * 1.965e9 / 1e9)
+    assert r["frac"] == pytest.approx(3.0e11 / (1.306 * 148 * 1.965e9))
+    assert bench.fused_roofline(1.0, {"sm_mhz": None, "sm_max_mhz": None}) is None
