@@ -353,6 +353,23 @@ def run_direct(fns: Sequence[Integrand], seed: int, trials: int,
     return (out, secs.value) if return_seconds else out
 
 
+def parameter_scan(program: "Program", params: Dict[str, float], name: str, values: Sequence[float],
+                   trials: int, seed: int, *, low=None, high=None, n_samples: int = 10000,
+                   devices: Optional[Sequence[int]] = None):
+    """parameter_scan (ref include/mcbatch/batch.hpp:76-81, src/batch.cpp:335-367): the
+    template program once per value of parameter `name` (integrand_index = the value's
+    position, as in the reference's `name#i` job), run as one batch.  Returns the
+    (len(values), trials) per-trial array and one (mean, trial_stddev, n_ok) per value."""
+    if name not in program.param_names:
+        raise ValueError(f"parameter '{name}' is not a parameter of the template")
+    if len(values) == 0:
+        raise ValueError("no values to scan")
+    fns = [program.integrand({**params, name: float(v)}, low=low, high=high, n_samples=n_samples, index=i)
+           for i, v in enumerate(values)]
+    out = run_direct(fns, seed, trials, devices)
+    return out, [summarize_trials(row) for row in out]
+
+
 def direct_mc(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, device: int = 0):
     st = TrialStats()
     _check(lib.mcb_direct_mc(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st)))

@@ -400,3 +400,27 @@ def test_wide_random_programs_vs_reference_golden(gpu):
                 assert abs(st.std_error - se) <= 1e-9 * se + 1e-300, (jit, c["source"])
         finally:
             gpu.program_jit(1)
+
+
+def test_parameter_scan_arguments(mcb):
+    p = mcb.Program("a*x1 + b", 1, ["a", "b"])
+    with pytest.raises(ValueError, match="not a parameter"):
+        mcb.parameter_scan(p, {"a": 1.0, "b": 0.0}, "c", [1.0], 2, 1)
+    with pytest.raises(ValueError, match="no values"):
+        mcb.parameter_scan(p, {"a": 1.0, "b": 0.0}, "a", [], 2, 1)
+
+
+@pytest.mark.gpu
+def test_parameter_scan_matches_reference(gpu):
+    """parameter_scan (ref src/batch.cpp:335-367) = run_batch of the expanded job: the
+    reference's own run_batch on the same sources, value by value."""
+    src = "cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))"
+    p = gpu.Program(src, 4, ["k"])
+    ks = [0.5 + 0.37 * i for i in range(24)]
+    out, summaries = gpu.parameter_scan(p, {}, "k", ks, 3, 77, n_samples=40_000)
+    fns = [p.integrand({"k": k}, n_samples=40_000, index=i) for i, k in enumerate(ks)]
+    ref, mean, _, _, _ = _oracle.ref_run_batch(fns, 77, 3, sources=[src.replace("k", repr(k)) for k in ks])
+    assert np.array_equal(out["n_samples"], ref["n_samples"])
+    assert np.all(np.abs(out["value"] - ref["value"]) <= 1e-12 + 1e-9 * np.abs(ref["value"]))
+    assert np.allclose([s[0] for s in summaries], mean, rtol=1e-9, atol=1e-12)
+    assert all(s[2] == 3 for s in summaries)
