@@ -397,22 +397,14 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
       for (uint32_t j = 0; j < f.dim; ++j) d.width[j] = d.width[j] * kTwoM64;
     }
     p.variant = (unit_dom ? kUnitDomain : 0) | (unit_coef ? kUnitCoef : 0);
-    // NOSHIFT: the argument sweeps >= 0.05 rad over the domain, so the
-    // integrand is far from constant and sum f^2 - (sum f)^2/n does not
-    // cancel; a (near-)constant integrand keeps the shift (exact 0 variance).
-    if (harm) {
-      double sweep = 0.0;
-      for (uint32_t j = 0; j < f.dim; ++j)  // over one cell when stratified
-        sweep += std::fabs(f.family == MCB_FAMILY_HARMONIC ? f.k[0] : f.k[j]) *
-                 (f.high[j] - f.low[j]) / cell_k;
-      if (sweep >= 0.05 && std::fabs(f.a) + std::fabs(f.b) > 0.0) p.variant |= kNoShift;
-    }
+    // direct harmonic: the shift rides in the CTA's table (kFoldShift), so
+    // g = f - c costs nothing extra; cells use a per-tile shift instead
+    if (harm && !strat) p.variant |= kFoldShift;
   } else {
     p.variant = kSafe;
   }
   if (!harm) p.variant &= ~kUnitCoef;
   if (strat) p.variant |= kStrat;
-  if (tree_cells) p.variant &= ~kNoShift;  // cells shrink: keep the per-tile shift
   if (stratified(f) && d.spc <= kWarpTileMaxSpc) {
     // small cells: a lane per cell on large grids (unit-coefficient or no
     // table), else a warp per cell
@@ -432,7 +424,6 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
     const double c = host_eval(f, mid);
     d.shift = std::isfinite(c) && std::fabs(c) < 1e300 ? c : 0.0;
   }
-  if (p.variant & kNoShift) d.shift = 0.0;  // the kernel accumulates f itself
   return p;
 }
 

@@ -2,9 +2,9 @@
 // table over the fused kernel instantiations (kernels.cuh, direct_*.cu), the
 // tile-table expansion, the ordered combine and the test/measurement hooks.
 //
-// K4 k_combine: one thread per (integrand, trial) sums its chunk partials in
-//    ascending chunk order (src/estimator.cpp:55-73 ordering) and forms the
-//    McEstimate fields.  Deterministic: no float atomics anywhere, reduction
+// K4 k_combine: one warp per (integrand, trial) merges its chunk partials in
+//    ascending chunk order (Chan, as ChunkAccum::merge, src/estimator.cpp:20-34,
+//    55-73) and forms the McEstimate fields.  Deterministic: no float atomics anywhere, reduction
 //    trees are fixed, so results do not depend on the GPU count or on the
 //    order in which the hardware schedules CTAs.
 #include <cuda_runtime.h>
@@ -94,8 +94,8 @@ __device__ __forceinline__ void merge_tile(Accum& a, const TilePartial& p) {
 }
 
 // K4: one WARP per (integrand, trial).
-//  * direct: lane 0 sums the chunk partials in ascending chunk order and
-//    forms the McEstimate (reduce_chunks, src/estimator.cpp:55-73);
+//  * direct: lane 0 merges the chunk partials (Chan) in ascending chunk
+//    order and forms the McEstimate (reduce_chunks, src/estimator.cpp:55-73);
 //  * cell-structured (stratified grid, tree round): lanes take cells
 //    c = lane, lane + 32, ...; each cell's chunks merge (Chan) into the cell's
 //    own direct_mc estimate.  Tree rounds store it per cell; stratified
@@ -205,15 +205,12 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
     return;
   }
   if (lane != 0) return;
-  double s1 = 0.0, s2 = 0.0;
-  uint64_t n = 0, nb = 0;
-  for (uint32_t c = 0; c < F.n_chunks; ++c) {
-    const TilePartial p = part[base + c];
-    s1 = __dadd_rn(s1, p.s1);
-    s2 = __dadd_rn(s2, p.s2);
-    n += p.n_finite;
-    nb += p.n_nonfinite;
-  }
+  // reduce_chunks: ChunkAccum::merge of the chunk partials in ascending chunk
+  // order (ref src/estimator.cpp:20-34,55-73); each tile's own (mean, m2)
+  // about its shift, so no cancellation builds up across the chunks
+  Accum a;
+  for (uint32_t c = 0; c < F.n_chunks; ++c) merge_tile(a, part[base + c]);
+  const uint64_t n = a.n, nb = a.nn;
   st.n_samples = n + nb;
   st.n_nonfinite = nb;
   st.nonfinite_warning = double(nb) > MCB_NONFINITE_WARN_FRACTION * double(n + nb) ? 1u : 0u;
@@ -223,15 +220,10 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
     st.std_error = 0.0;
   } else {
     st.status = MCB_TRIAL_OK;
-    const double dn = double(n);
-    const double dev_mean = __ddiv_rn(s1, dn);
-    const double mean = __dadd_rn(F.shift, dev_mean);
-    st.value = __dmul_rn(F.volume, mean);
+    st.value = __dmul_rn(F.volume, a.mean);
     if (n >= 2) {
-      double m2 = __dsub_rn(s2, __dmul_rn(s1, dev_mean));
-      m2 = m2 > 0.0 ? m2 : 0.0;
-      const double var = __ddiv_rn(m2, double(n - 1));
-      st.std_error = __dmul_rn(F.volume, __dsqrt_rn(__ddiv_rn(var, dn)));
+      const double var = __ddiv_rn(a.m2, double(n - 1));
+      st.std_error = __dmul_rn(F.volume, __dsqrt_rn(__ddiv_rn(var, double(n))));
     } else {
       st.std_error = __longlong_as_double(0x7FF0000000000000ll);  // +inf
     }

@@ -8,19 +8,13 @@ namespace detail {
 template <int D>
 static void put_harmonic(Table& t) {
   constexpr int F = MCB_FAMILY_HARMONIC;
-  t.put<F, D, 0>();
-  t.put<F, D, kUnitDomain>();
-  t.put<F, D, kUnitCoef>();
-  t.put<F, D, kUnitCoef | kUnitDomain>();
-  t.put<F, D, kNoShift>();
-  t.put<F, D, kNoShift | kUnitDomain>();
-  t.put<F, D, kNoShift | kUnitCoef>();
-  t.put<F, D, kNoShift | kUnitCoef | kUnitDomain>();
+  t.put<F, D, kFoldShift>();
+  t.put<F, D, kFoldShift | kUnitDomain>();
+  t.put<F, D, kFoldShift | kUnitCoef>();
+  t.put<F, D, kFoldShift | kUnitCoef | kUnitDomain>();
   t.put<F, D, kSafe>();
   t.put_run<F, D, 0>();
   t.put_run<F, D, kUnitCoef>();
-  t.put_run<F, D, kNoShift>();
-  t.put_run<F, D, kNoShift | kUnitCoef>();
   t.put_run<F, D, kSafe>();
 }
 

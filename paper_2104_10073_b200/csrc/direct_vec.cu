@@ -8,13 +8,10 @@ namespace detail {
 template <int D>
 static void put_vec(Table& t) {
   constexpr int F = MCB_FAMILY_HARMONIC_VEC;
-  t.put<F, D, 0>();
-  t.put<F, D, kUnitDomain>();
-  t.put<F, D, kNoShift>();
-  t.put<F, D, kNoShift | kUnitDomain>();
+  t.put<F, D, kFoldShift>();
+  t.put<F, D, kFoldShift | kUnitDomain>();
   t.put<F, D, kSafe>();
   t.put_run<F, D, 0>();
-  t.put_run<F, D, kNoShift>();
   t.put_run<F, D, kSafe>();
 }
 

@@ -43,6 +43,14 @@ __device__ __forceinline__ void build_trig_table(TrigAB* ab, double a, double b)
     ab[m] = dev::trig_ab<UNIT_COEF>(dev::g_trig_dev[m], a, b);
 }
 
+// kFoldShift table: {A_m - c, B_m, A_m} per entry (mcb_device.cuh).
+template <bool UNIT_COEF>
+__device__ __forceinline__ void build_trig_table_shifted(dev::TrigABS* tab, double a, double b,
+                                                         double c) {
+  for (int m = threadIdx.x; m < 512; m += blockDim.x)
+    tab[m] = dev::trig_abs_entry(dev::g_trig_dev[m], a, b, c, UNIT_COEF);
+}
+
 template <int FAM, int D, int V>
 __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
     k_direct(const FnDesc* __restrict__ fns, const uint32_t* __restrict__ tile_fn, uint64_t tile0,
@@ -50,10 +58,11 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
   constexpr bool UNIT_DOM = (V & kUnitDomain) != 0;
   constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
   constexpr bool SAFE = (V & kSafe) != 0;
-  constexpr bool NOSHIFT = (V & kNoShift) != 0;
+  constexpr bool FOLD = (V & kFoldShift) != 0;
   constexpr bool STRAT = (V & kStrat) != 0;
   constexpr bool HARM = FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC;
   constexpr bool TABLE = HARM && !SAFE;
+  static_assert(!FOLD || (TABLE && !STRAT), "folded shift: FAST harmonic, direct method");
 
   const uint64_t tile = tile0 + blockIdx.x;
   const uint32_t fi = __ldg(tile_fn + tile);
@@ -77,15 +86,19 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
   const uint32_t pairs = (count + 1) >> 1;
   const PhiloxPrefix P =
       dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
-  __shared__ TrigAB ab[TABLE ? 512 : 1];
+  __shared__ TrigAB ab[TABLE && !FOLD ? 512 : 1];
+  __shared__ dev::TrigABS abs_tab[FOLD ? 512 : 1];
   if (TABLE) {
-    build_trig_table<UNIT_COEF>(ab, f.a, f.b);
+    if (FOLD)
+      build_trig_table_shifted<UNIT_COEF>(abs_tab, f.a, f.b, f.shift);
+    else
+      build_trig_table<UNIT_COEF>(ab, f.a, f.b);
     __syncthreads();
   }
   // STRAT: per-tile shift = f(first sample of the tile); tiles merge by
   // Chan's formula in k_combine, so cells (often near-constant) keep an
   // exactly zero variance when f is constant on them.
-  if (STRAT && !NOSHIFT) {
+  if (STRAT) {
     __shared__ double s_shift;
     if (threadIdx.x == 0) {
       double st0, st1;
@@ -114,13 +127,20 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
     pbase += kStep;
     double b0, b1;
     dev::gen_pair<FAM, D, UNIT_DOM, SAFE>(f, P, pbase, b0, b1);
-    const double f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a0);
-    const double f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a1);
+    double f0, f1, g0, g1;
+    if constexpr (FOLD) {  // g = f - shift straight from the folded table
+      g0 = dev::finish_shifted<FAM>(f, c_trig, abs_tab, a0);
+      g1 = dev::finish_shifted<FAM>(f, c_trig, abs_tab, a1);
+      f0 = f1 = 0.0;
+    } else {
+      f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a0);
+      f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a1);
+      g0 = __dsub_rn(f0, f.shift);
+      g1 = __dsub_rn(f1, f.shift);
+    }
     a0 = b0;
     a1 = b1;
     const bool has1 = 2 * q + 1 < count;
-    double g0 = NOSHIFT ? f0 : __dsub_rn(f0, f.shift);
-    double g1 = NOSHIFT ? f1 : __dsub_rn(f1, f.shift);
     if (SAFE) {
       const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
       nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
@@ -163,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
     TilePartial p;
     p.s1 = t1;
     p.s2 = t2;
-    p.shift = NOSHIFT ? 0.0 : f.shift;
+    p.shift = f.shift;
     p.n_nonfinite = SAFE ? tb : 0u;
     p.n_finite = count - p.n_nonfinite;
     part[tile] = p;
@@ -190,7 +210,6 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
                   TilePartial* __restrict__ part) {
   constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
   constexpr bool SAFE = (V & kSafe) != 0;
-  constexpr bool NOSHIFT = (V & kNoShift) != 0;
   constexpr bool HARM = FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC;
   constexpr bool TABLE = HARM && !SAFE;
   static_assert((V & kStrat) && (V & kWarpTile), "cell-structured warp-tile variant");
@@ -224,8 +243,8 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
   uint32_t nbad = 0;
   auto add = [&](uint32_t q, double f0, double f1) {
     const bool has1 = 2 * q + 1 < count;
-    double g0 = NOSHIFT ? f0 : __dsub_rn(f0, f.shift);
-    double g1 = NOSHIFT ? f1 : __dsub_rn(f1, f.shift);
+    double g0 = __dsub_rn(f0, f.shift);
+    double g1 = __dsub_rn(f1, f.shift);
     if (SAFE) {
       const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
       nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
@@ -249,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
       f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
       f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
     }
-    if (!NOSHIFT) {
+    {
       const double c = __shfl_sync(0xFFFFFFFFu, f0, 0);
       f.shift = finite64(c) ? c : 0.0;
     }
@@ -287,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, warp_tile_min_blocks(D, V))
     TilePartial p;
     p.s1 = s1;
     p.s2 = s2;
-    p.shift = NOSHIFT ? 0.0 : f.shift;
+    p.shift = f.shift;
     p.n_nonfinite = SAFE ? nbad : 0u;
     p.n_finite = count - p.n_nonfinite;
     part[tile] = p;
@@ -310,7 +329,6 @@ __global__ void __launch_bounds__(kLaneAlign, 8 * warp_tile_min_blocks(D, V))
                   TilePartial* __restrict__ part) {
   constexpr bool UNIT_COEF = (V & kUnitCoef) != 0;
   constexpr bool SAFE = (V & kSafe) != 0;
-  constexpr bool NOSHIFT = (V & kNoShift) != 0;
   constexpr bool HARM = FAM == MCB_FAMILY_HARMONIC || FAM == MCB_FAMILY_HARMONIC_VEC;
   constexpr bool TABLE = HARM && !SAFE;
   static_assert((V & kStrat) && (V & kLaneCell) && !(V & kWarpTile), "cell-per-lane variant");
@@ -333,8 +351,8 @@ __global__ void __launch_bounds__(kLaneAlign, 8 * warp_tile_min_blocks(D, V))
   uint32_t nbad = 0;
   auto add = [&](uint32_t q, double f0, double f1) {
     const bool has1 = 2 * q + 1 < count;
-    double g0 = NOSHIFT ? f0 : __dsub_rn(f0, f.shift);
-    double g1 = NOSHIFT ? f1 : __dsub_rn(f1, f.shift);
+    double g0 = __dsub_rn(f0, f.shift);
+    double g1 = __dsub_rn(f1, f.shift);
     if (SAFE) {
       const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
       nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
@@ -354,7 +372,7 @@ __global__ void __launch_bounds__(kLaneAlign, 8 * warp_tile_min_blocks(D, V))
     dev::gen_pair<FAM, D, false, SAFE>(f, P, 0, x0, x1);
     const double f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x0);
     const double f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, x1);
-    if (!NOSHIFT) f.shift = finite64(f0) ? f0 : 0.0;
+    f.shift = finite64(f0) ? f0 : 0.0;
     add(0, f0, f1);
   }
   uint32_t q = 1;
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(kLaneAlign, 8 * warp_tile_min_blocks(D, V))
   TilePartial p;
   p.s1 = s1;
   p.s2 = s2;
-  p.shift = NOSHIFT ? 0.0 : f.shift;
+  p.shift = f.shift;
   p.n_nonfinite = SAFE ? nbad : 0u;
   p.n_finite = count - p.n_nonfinite;
   part[tile] = p;
@@ -396,15 +414,28 @@ __global__ void k_debug_eval(const FnDesc* __restrict__ fn, uint32_t trial, uint
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const FnDesc f = *fn;
   const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, chunk, trial);
-  __shared__ TrigAB ab[TABLE ? 512 : 1];
+  constexpr bool FOLD = (V & kFoldShift) != 0;
+  __shared__ TrigAB ab[TABLE && !FOLD ? 512 : 1];
+  __shared__ dev::TrigABS abs_tab[FOLD ? 512 : 1];
   if (TABLE) {
-    build_trig_table<UNIT_COEF>(ab, f.a, f.b);
+    if (FOLD)
+      build_trig_table_shifted<UNIT_COEF>(abs_tab, f.a, f.b, f.shift);
+    else
+      build_trig_table<UNIT_COEF>(ab, f.a, f.b);
     __syncthreads();
   }
   if (i >= n_pairs) return;
   double f0, f1;
-  dev::eval_pair<FAM, D, (V & kUnitDomain) != 0, UNIT_COEF, SAFE>(f, c_trig, ab, P, first_pair + i,
-                                                                   f0, f1);
+  if constexpr (FOLD) {  // the fused kernel's g, reported as g + shift
+    double st0, st1;
+    dev::gen_pair<FAM, D, (V & kUnitDomain) != 0, SAFE>(
+        f, P, uint64_t(dev::kM0) * uint64_t((first_pair + i) * uint32_t(D)), st0, st1);
+    f0 = __dadd_rn(dev::finish_shifted<FAM>(f, c_trig, abs_tab, st0), f.shift);
+    f1 = __dadd_rn(dev::finish_shifted<FAM>(f, c_trig, abs_tab, st1), f.shift);
+  } else {
+    dev::eval_pair<FAM, D, (V & kUnitDomain) != 0, UNIT_COEF, SAFE>(f, c_trig, ab, P, first_pair + i,
+                                                                     f0, f1);
+  }
   out[2 * uint64_t(i)] = f0;
   out[2 * uint64_t(i) + 1] = f1;
 }

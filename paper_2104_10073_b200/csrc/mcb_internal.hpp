@@ -34,8 +34,9 @@ enum Variant : int {
   kSafe = 4,        // plain parameters, libdevice sincos, non-finite samples
                     // counted and skipped (used when the host cannot prove
                     // the FAST preconditions, see capi.cpp prepare())
-  kNoShift = 8,     // harmonic FAST: accumulate f itself (the host proved the
-                    // integrand far from constant, so no cancellation)
+  kFoldShift = 8,   // harmonic FAST, direct (not kStrat): the per-integrand
+                    // shift c is folded into the CTA's table (A_m - c), so
+                    // g = f - c costs no extra FP64 operation (mcb_device.cuh)
   kStrat = 16,      // STRATIFIED method: tiles are (trial, cell, chunk), the
                     // cell rectangle is derived on the device (grid_cell)
   kWarpTile = 32,   // with kStrat, small cells: one WARP per tile, so a CTA

@@ -10,6 +10,10 @@
 //  4. the table-form sin/cos (the kernel's reduction): absolute error < 3 * 2^-53
 //  5. a*cos t + b*sin t in table form: error < 2.5 * max(|a|,|b|) * 2^-52
 //  6. trig_table.inc holds correctly rounded cos/sin of m*pi/256
+//  7. the folded-shift form g = a*cos t + b*sin t - c (kFoldShift):
+//     error < 3.5 * max(|a|,|b|,|c|) * 2^-52 per sample (a rounded f minus c:
+//     ~2.4); the per-entry part, A_m - c, is correctly rounded, so the only
+//     systematic error a Monte Carlo mean can pick up is <= 0.5 ulp
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -119,6 +123,51 @@ int main() {
   }
   std::printf("a cos t + b sin t: max error %.3f x max(|a|,|b|) 2^-52; unit form %.3f x 2^-52\n", max_h, max_u);
   CHECK(max_h < 2.5 && max_u < 2.0, "harmonic value accuracy %.3f %.3f", max_h, max_u);
+  // 7. folded shift: g = A_m cm1(r) + (B_m sin r + (A_m - c)) against the exact
+  //    a cos t + b sin t - c, c anywhere in the integrand's range
+  double max_g = 0, max_gu = 0, max_sub = 0;
+  for (int i = 0; i < 2000000; ++i) {
+    const double t = std::uniform_real_distribution<double>(-700, 700)(rng);
+    const double a = std::uniform_real_distribution<double>(-3, 3)(rng);
+    const double b = std::uniform_real_distribution<double>(-3, 3)(rng);
+    const double c = std::uniform_real_distribution<double>(-1, 1)(rng) * (std::fabs(a) + std::fabs(b));
+    const double cu = std::uniform_real_distribution<double>(-1.5, 1.5)(rng);
+    double r, s, cm1;
+    uint32_t m;
+    trig_reduce(K, t, r, m);
+    trig_sc_m1(K, r, s, cm1);
+    const TrigAB e = trig_ab<false>(g_trig_host[m], a, b);
+    const double g = trig_combine_shifted(trig_abs_entry(g_trig_host[m], a, b, c, false), s, cm1);
+    const long double ex =
+        (long double)a * cosl((long double)t) + (long double)b * sinl((long double)t) - (long double)c;
+    const double scale = std::fmax(std::fmax(std::fabs(a), std::fabs(b)), std::fabs(c));
+    max_g = std::fmax(max_g, double(std::fabs((long double)g - ex)) / (scale * 0x1p-52));
+    {  // the unfolded alternative: rounded f, then a rounded subtraction
+      double s0, c0;
+      trig_sc(K, r, s0, c0);
+      const double sub = trig_combine(e, s0, c0) - c;
+      max_sub = std::fmax(max_sub, double(std::fabs((long double)sub - ex)) / (scale * 0x1p-52));
+    }
+    const double gu = trig_combine_shifted(trig_abs_entry(g_trig_host[m], 1.0, 1.0, cu, true), s, cm1);
+    const long double exu = cosl((long double)t) + sinl((long double)t) - (long double)cu;
+    max_gu = std::fmax(max_gu, double(std::fabs((long double)gu - exu)) / (std::fmax(1.0, std::fabs(cu)) * 0x1p-52));
+  }
+  std::printf("folded shift a cos t + b sin t - c: max error %.3f x max(|a|,|b|,|c|) 2^-52 "
+              "(unfolded f - c: %.3f); unit form %.3f\n", max_g, max_sub, max_gu);
+  CHECK(max_g < 3.5 && max_gu < 3.5, "folded-shift accuracy %.3f %.3f (unfolded %.3f)",
+        max_g, max_gu, max_sub);
+  // constant integrand (t = 0 on the whole domain, c = f(0)): g is exactly 0
+  {
+    double r, s, cm1;
+    uint32_t m;
+    trig_reduce(K, 0.0, r, m);
+    trig_sc_m1(K, r, s, cm1);
+    const double c = 0.75 * g_trig_host[0].c + -1.25 * g_trig_host[0].s;  // a*cos 0 + b*sin 0
+    CHECK(trig_combine_shifted(trig_abs_entry(g_trig_host[0], 0.75, -1.25, c, false), s, cm1) == 0.0,
+          "folded constant");
+    CHECK(trig_combine_shifted(trig_abs_entry(g_trig_host[0], 1.0, 1.0, 1.0, true), s, cm1) == 0.0,
+          "folded constant, unit form");
+  }
   // 6. the table itself: entries equal the correctly rounded cos/sin
   for (int mm = 0; mm < 512; ++mm) {
     const long double ang = (long double)mm * 3.14159265358979323846264338327950288L / 256.0L;
