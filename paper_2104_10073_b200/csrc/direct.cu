@@ -78,7 +78,9 @@ __device__ __forceinline__ void merge_tile(Accum& a, const TilePartial& p) {
   const double dev_b = __ddiv_rn(p.s1, n_b);
   const double mean_b = __dadd_rn(p.shift, dev_b);
   double m2_b = __dsub_rn(p.s2, __dmul_rn(p.s1, dev_b));
-  m2_b = m2_b > 0.0 ? m2_b : 0.0;
+  // rounding can leave a tiny negative m2 (clamp to 0); inf - inf = NaN only
+  // when the sum of squares overflowed, where Welford's m2 is +inf too
+  m2_b = m2_b > 0.0 ? m2_b : (m2_b == m2_b ? 0.0 : __longlong_as_double(0x7FF0000000000000ll));
   if (a.n == 0) {
     a.n = p.n_finite;
     a.mean = mean_b;

@@ -35,3 +35,13 @@ def gpu(mcb):
     if mcb.device_count() < 1:
         pytest.fail("no CUDA device visible: -m gpu tests need a B200 (no CPU fallback exists)")
     return mcb
+
+
+def pytest_terminal_summary(terminalreporter):
+    """Largest deviation / tolerance per parity comparison (tests/_deviation.py)."""
+    from tests import _deviation
+    lines = _deviation.summary_lines()
+    if lines:
+        terminalreporter.write_sep("-", "parity margins: max |gpu - ref| / tolerance")
+        for line in lines:
+            terminalreporter.write_line(line)

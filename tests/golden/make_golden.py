@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import math
 import os
 import sys
 
@@ -177,6 +178,11 @@ def main():
 
     # 9. stratified_mc standalone (src/estimator.cpp:161-182) with leaves
     g["stratified_mc"] = make_stratified_mc_goldens()
+
+    # 10. config scale: C4 / C5 subsets at the configs' own 1e7 samples (153
+    # chunks per (integrand, trial)) and near-constant harmonic cases where
+    # sum g^2 - (sum g)^2/n would cancel without a good shift
+    g["config_scale"] = make_config_scale_goldens(ref)
 
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(g, fh, indent=1)
@@ -379,6 +385,63 @@ def make_wide_program_goldens(ref):
                     "seed": seed, "index": index, "trial": trial, "chunk_base": cb,
                     "values": [H(float(x)) for x in v], "estimate": stats_json(st)})
     return out
+
+
+# C4 (parameter_scan of the 7-D harmonic, k_i = 0.01 (i+1)): 8 of the 4096
+# values, k = 0.01 ... 40.96, with their scan positions as integrand indices.
+C4_SUBSET = [0, 4, 19, 99, 511, 1023, 2047, 4095]
+# C5 (10^4 integrands cycling abs2/abs3/harmonic d = 2..7): n = 617 i cycles
+# all 8 kinds twice (617 = 1 mod 8).
+C5_SUBSET = [617 * i for i in range(16)]
+
+
+def threshold_cases():
+    """Near-constant harmonic integrands (argument sweep 0.05-0.1 rad at an
+    extremum of a*cos + b*sin): var/mean^2 ~ 1e-7, the regime where an
+    unshifted sum of squares loses the std_error."""
+    q = math.pi / 4
+    return [
+        mcb.harmonic(1.0, 1, a=1.0, b=0.0, low=[0.0], high=[0.05], n_samples=2_000_000, index=0),
+        mcb.harmonic(1.0, 1, a=1.0, b=0.0, low=[0.0], high=[0.1], n_samples=2_000_000, index=1),
+        mcb.harmonic(0.05 / 4, 4, a=1.0, b=0.0, n_samples=2_000_000, index=2),
+        mcb.harmonic(0.1 / 4, 4, a=1.0, b=0.0, n_samples=2_000_000, index=3),
+        mcb.harmonic(1.0, 2, a=0.0, b=1.0, low=[q - 0.0125] * 2, high=[q + 0.0125] * 2, n_samples=2_000_000,
+                     index=4),
+        mcb.harmonic(0.1 / 7, 7, a=1.0, b=0.0, n_samples=2_000_000, index=5),
+        mcb.harmonic(1.0, 1, a=1.0, b=0.0, low=[-0.025], high=[0.025], n_samples=2_000_000, index=6),
+        mcb.make_integrand(mcb.FAMILY_HARMONIC_VEC, 3, k=[0.01, 0.02, 0.005], a=2.0, b=0.0,
+                           n_samples=2_000_000, index=7),
+        mcb.harmonic(1.0, 4, a=3.0, b=0.5, low=[0.1] * 4, high=[0.1125] * 4, n_samples=2_000_000, index=8),
+    ]
+
+
+def config_scale_specs():
+    c4, seed4, _ = workloads.c4(samples=10_000_000)
+    c5, seed5, _ = workloads.c5(samples=10_000_000, n_fns=C5_SUBSET[-1] + 1)
+    return ([("c4", c4[i], seed4) for i in C4_SUBSET] + [("c5", c5[n], seed5) for n in C5_SUBSET] +
+            [("threshold", f, 97) for f in threshold_cases()])
+
+
+def make_config_scale_goldens(ref):
+    from concurrent.futures import ThreadPoolExecutor
+    specs = config_scale_specs()
+    trials = 2
+
+    def one(job):
+        (_, f, seed), t = job
+        st = mcb.TrialStats()
+        rc = ref.ref_direct_mc(mcb.to_dsl(f).encode(), ctypes.byref(f), seed, t, 0, ctypes.byref(st))
+        assert rc == 0, ref.ref_last_error()
+        return stats_json(st)
+
+    jobs = [(sp, t) for sp in specs for t in range(trials)]
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:  # ctypes drops the GIL
+        res = list(ex.map(one, jobs))
+    out = []
+    for i, (group, f, seed) in enumerate(specs):
+        out.append({"group": group, "desc": desc_json(f), "seed": seed,
+                    "per_trial": res[i * trials:(i + 1) * trials]})
+    return {"trials": trials, "chunk_base": 0, "cases": out}
 
 
 def _as_stats(row):
