@@ -220,8 +220,11 @@ MCB_API size_t mcb_program_param_name(const mcb_program* program, uint32_t i, ch
  * [0, trials), StreamKey {seed, integrand_index, t, chunk}, by each
  * integrand's method (DIRECT, STRATIFIED, TREE).
  * `out` is n_fns*trials, row-major by integrand.  Devices: `devices` lists
- * CUDA ordinals (NULL/0 = device 0); one host thread per entry, integrands
- * sharded by mcb_partition; results are byte-identical for any device list.
+ * CUDA ordinals (NULL/0 = device 0); one host thread per entry.  With one
+ * device every integrand runs there; with several, the (integrand, trial)
+ * pairs of direct and stratified integrands are sharded by LPT on cost (tree
+ * integrands: whole trees by budget).  Results are byte-identical for any
+ * device list.
  * Synchronous.  `seconds` (may be NULL) receives the wall time of the
  * sampling phase (reference BatchResult.total_seconds). */
 MCB_API mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,

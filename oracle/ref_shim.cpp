@@ -218,6 +218,44 @@ int ref_harmonic_job(std::uint32_t n_count, std::uint64_t samples, double* k_out
   }
 }
 
+// Timing leg of bench.py (reference arm and cpu_baseline): the reference's
+// own make_harmonic_job(n_total, samples) (src/job_io.cpp:355-376), of which
+// the integrands at positions first, first + stride, ... (count of them) form
+// the job that the reference's run_batch (src/batch.cpp:195-333) runs with
+// `workers` threads (0 = all hardware threads, batch.cpp:56-60).  The subset
+// keeps each integrand's source, k, domain and budget; its integrand_index is
+// its position in the subset (the reference's rule), so the streams differ
+// from the full job's while the per-sample cost is the same.  Returns
+// BatchResult.total_seconds (validate/compile excluded, batch.cpp:293-299),
+// the worker count the reference resolved and the number of integrands whose
+// trials all succeeded.
+int ref_run_harmonic(std::uint32_t n_total, std::uint64_t samples, std::uint32_t first,
+                     std::uint32_t count, std::uint32_t stride, std::uint32_t workers,
+                     double* seconds, std::uint32_t* workers_used, std::uint32_t* n_ok) {
+  try {
+    JobSpec full = make_harmonic_job(n_total, samples);
+    JobSpec job;
+    job.seed = full.seed;
+    job.trials = full.trials;
+    job.workers = workers;
+    for (std::uint32_t i = 0; i < count; ++i) {
+      std::size_t pos = std::size_t(first) + std::size_t(i) * stride;
+      if (pos >= full.integrands.size()) break;
+      job.integrands.push_back(full.integrands[pos]);
+    }
+    BatchResult br = run_batch(job);
+    std::uint32_t ok = 0;
+    for (const IntegrandResult& r : br.per_integrand) ok += r.ok ? 1u : 0u;
+    *seconds = br.total_seconds;
+    *workers_used = resolve_workers(workers);
+    *n_ok = ok;
+    return int(job.integrands.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // evaluate (src/expr.cpp:520-553) of an arbitrary source with named params.
 int ref_eval_source(const char* source, std::uint32_t dim, const char* const* names,
                     const double* values, std::size_t n_params, const double* pts,

@@ -132,11 +132,69 @@ void lpt(const mcb_integrand* fns, size_t n, uint32_t trials, int shards, uint32
   }
 }
 
+// Multi-device form of run_sharded: the units are (integrand, trial) pairs,
+// not whole integrands, so a job of a few integrands still fills every device
+// (C1 = 100 integrands on 8 GPUs: 125 pairs each instead of 13 vs 12
+// integrands).  A pair runs as a one-trial sub-integrand whose trial_base is
+// its trial, so its key, counters and tile structure — and hence its
+// McEstimate — are exactly those of the single-device plan (SURVEY.md §8(e):
+// a (fn, trial, chunk) unit depends only on (seed, integrand_index, trial,
+// chunk, spec), ref tests/test_batch.cpp:137-158).  LPT over the pairs by
+// cost, ties in (integrand, trial) order; one host thread per device.
+mcb_status run_sharded_trials(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
+                              const std::vector<int>& devs, mcb_trial_stats* out) {
+  const size_t n_units = n_fns * size_t(trials);
+  std::vector<double> cost(n_fns);
+  for (size_t i = 0; i < n_fns; ++i) cost[i] = double(trial_samples(fns[i])) * sample_cost(fns[i]);
+  std::vector<size_t> order(n_units);
+  std::iota(order.begin(), order.end(), size_t(0));
+  std::stable_sort(order.begin(), order.end(),
+                   [&](size_t a, size_t b) { return cost[a / trials] > cost[b / trials]; });
+  std::vector<std::vector<size_t>> mine(devs.size());
+  std::vector<double> load(devs.size(), 0.0);
+  for (size_t u : order) {
+    size_t best = 0;
+    for (size_t s = 1; s < load.size(); ++s)
+      if (load[s] < load[best]) best = s;
+    mine[best].push_back(u);
+    load[best] += cost[u / trials];
+  }
+  std::vector<mcb_status> status(devs.size(), MCB_OK);
+  std::vector<std::string> errors(devs.size());
+  auto work = [&](size_t w) {
+    std::vector<size_t>& units = mine[w];
+    if (units.empty()) return;
+    std::sort(units.begin(), units.end());  // job order within the device
+    std::vector<mcb_integrand> sub(units.size());
+    std::vector<uint32_t> tb(units.size()), cb(units.size(), 0);
+    for (size_t r = 0; r < units.size(); ++r) {
+      sub[r] = fns[units[r] / trials];
+      tb[r] = uint32_t(units[r] % trials);
+    }
+    std::vector<mcb_trial_stats> res(units.size());
+    const mcb_status s = run_shard(sub.data(), sub.size(), seed, 1, devs[w], res.data(), cb.data(), tb.data());
+    status[w] = s;
+    if (s != MCB_OK) {
+      errors[w] = g_last_error;
+      return;
+    }
+    for (size_t r = 0; r < units.size(); ++r) out[units[r]] = res[r];
+  };
+  std::vector<std::thread> pool;
+  for (size_t w = 0; w < devs.size(); ++w) pool.emplace_back(work, w);
+  for (auto& th : pool) th.join();
+  for (size_t w = 0; w < devs.size(); ++w)
+    if (status[w] != MCB_OK) return fail(status[w], "device " + std::to_string(devs[w]) + ": " + errors[w]);
+  return MCB_OK;
+}
+
 // Shards integrands over `devs` by LPT, one host thread per device; results
 // land in `out` (n_fns * trials) by integrand.  Byte-identical for any list.
 mcb_status run_sharded(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
                        const std::vector<int>& devs, mcb_trial_stats* out, const uint32_t* chunk_bases,
                        const uint32_t* trial_bases) {
+  if (devs.size() > 1 && trials > 1 && !chunk_bases && !trial_bases)
+    return run_sharded_trials(fns, n_fns, seed, trials, devs, out);
   std::vector<uint32_t> shard(n_fns, 0);
   lpt(fns, n_fns, trials, int(devs.size()), shard.data());
   std::vector<mcb_status> status(devs.size(), MCB_OK);

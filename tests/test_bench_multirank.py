@@ -24,7 +24,7 @@ def _torchrun(extra):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--samples", "100000", "--n-fns", "200",
-           "--no-clocks", *extra]
+           "--no-clocks", "--c5-fns", "64", "--c5-samples", "100000", *extra]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -42,6 +42,14 @@ def test_bench_two_ranks(scaling):
     # value = samples of all ranks per step / the slowest rank's step time
     per_step = (2 * 200 if scaling == "weak" else 200) * 100_000 * 10
     assert line["value"] * line["ms_per_step"] / 1e3 == pytest.approx(per_step, rel=1e-9)
+    # e2e: rank 0 times the product's own scheduler over the whole job (both devices)
+    assert "devices=[0, 0]" in line["e2e"]["path"]
+    assert line["e2e"]["h2d_bytes_per_step"] == (2 * 200 if scaling == "weak" else 200) * 272
+    # configs[4] (C5) weak and strong, max over ranks
+    c5 = line["scaling_c5"]
+    assert c5["weak"]["integrands"] == 2 * 8 and c5["strong"]["integrands"] == 64
+    assert c5["weak"]["samples_per_s"] > 0 and c5["strong"]["samples_per_s"] > 0
+    assert line["config"]["integrands"] == (400 if scaling == "weak" else 200)
 
 
 def test_fused_roofline_arithmetic():
