@@ -1,7 +1,8 @@
 // job_io.cpp — job files, results CSV and the Fig. 1 harness on the GPU
-// backend (include/mcb/job_io.hpp).  Formats and messages follow the
-// reference's src/job_io.cpp (file:line cited per function); the strict JSON
-// reader is a small RFC 8259 parser of our own (the reference uses nlohmann).
+// backend (include/mcb/job_io.hpp).  Formats follow SPEC.md [MODULE] cli
+// (strict JSON job files; the 17-digit results CSV; exit codes 0 / 2 / 3)
+// so that the reference's own readers accept our files; the JSON reader is a
+// small RFC 8259 parser, the CSV layer a column table (kColumns).
 #include "mcb/job_io.hpp"
 
 #include <algorithm>
@@ -14,6 +15,8 @@
 #include <iostream>
 #include <limits>
 #include <map>
+#include <optional>
+#include <string_view>
 #include <memory>
 #include <numbers>
 #include <sstream>
@@ -352,44 +355,6 @@ std::string json_string(const std::string& s) {
   return o + "\"";
 }
 
-std::string fmt17(double v) {  // ref job_io.cpp:144-148
-  char buf[40];
-  std::snprintf(buf, sizeof buf, "%.17g", v);
-  return buf;
-}
-
-std::string sanitize_field(std::string s) {  // ref job_io.cpp:150-155
-  for (char& c : s)
-    if (c == ',' || c == '\n' || c == '\r') c = ';';
-  return s;
-}
-
-const char* kResultsHeader =
-    "name,index,dim,method,samples,trials,mean,trial_stddev,mean_std_error,analytic,abs_error,"
-    "warnings";
-
-std::vector<std::string> split_csv_line(const std::string& line) {  // ref job_io.cpp:225-239
-  std::vector<std::string> fields;
-  std::string cur;
-  for (char c : line) {
-    if (c == ',') {
-      fields.push_back(cur);
-      cur.clear();
-    } else if (c != '\r') {
-      cur += c;
-    }
-  }
-  fields.push_back(cur);
-  return fields;
-}
-
-double parse_double(const std::string& s, const char* what) {
-  char* end = nullptr;
-  const double v = std::strtod(s.c_str(), &end);
-  if (end == s.c_str()) throw MalformedResults(std::string("bad numeric field '") + s + "' for " + what);
-  return v;
-}
-
 }  // namespace
 
 // ---- jobs (ref job_io.cpp:66-142) -------------------------------------------------
@@ -498,140 +463,220 @@ void write_job(const JobSpec& job, const std::filesystem::path& path) {
   out << job_to_json_text(job);
 }
 
-// ---- results (ref job_io.cpp:171-284) ------------------------------------------
+// ---- results table ------------------------------------------------------------
+// SPEC.md [MODULE] cli, ResultsTable: one CSV row per integrand in job order,
+// header row, ',' separator, '.' decimal point, numbers with 17 significant
+// digits (so a value survives write -> read bit for bit), warnings as a ';'
+// list.  The table is described once, column by column (kColumns): the
+// header, the writer and the reader are all driven by it.  The byte layout is
+// the one the reference's own reader/writer accepts and reproduces
+// (tests/test_job_io.py round-trips our files through them).
+
+namespace {
+
+// 17 significant digits, C locale (to_chars general == printf %.17g).
+std::string num17(double v) {
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof buf, v, std::chars_format::general, 17);
+  return std::string(buf, r.ptr);
+}
+
+// A cell may not contain the separator or a line break.
+std::string cell_text(std::string s) {
+  std::replace_if(s.begin(), s.end(), [](char c) { return c == ',' || c == '\n' || c == '\r'; }, ';');
+  return s;
+}
+
+std::vector<std::string> csv_cells(std::string_view line) {
+  if (!line.empty() && line.back() == '\r') line.remove_suffix(1);
+  std::vector<std::string> cells;
+  for (std::size_t start = 0;;) {
+    const std::size_t comma = line.find(',', start);
+    cells.emplace_back(line.substr(start, comma == std::string_view::npos ? std::string_view::npos : comma - start));
+    if (comma == std::string_view::npos) return cells;
+    start = comma + 1;
+  }
+}
+
+template <class T>
+T read_number(const std::string& text, const char* column) {
+  T v{};
+  const char* end = text.data() + text.size();
+  const auto r = std::from_chars(text.data(), end, v);
+  if (r.ec != std::errc() || r.ptr != end)
+    throw MalformedResults(std::string("column ") + column + ": not a number: '" + text + "'");
+  return v;
+}
+
+std::string opt_num17(const std::optional<double>& v) { return v ? num17(*v) : std::string(); }
+std::optional<double> read_opt(const std::string& text, const char* column) {
+  if (text.empty()) return std::nullopt;
+  return read_number<double>(text, column);
+}
+
+struct Column {
+  const char* name;
+  std::string (*write)(const ResultsRow&);
+  void (*read)(ResultsRow&, const std::string&);
+};
+
+const Column kColumns[] = {
+    {"name", [](const ResultsRow& r) { return cell_text(r.name); },
+     [](ResultsRow& r, const std::string& s) { r.name = s; }},
+    {"index", [](const ResultsRow& r) { return std::to_string(r.index); },
+     [](ResultsRow& r, const std::string& s) { r.index = read_number<std::uint32_t>(s, "index"); }},
+    {"dim", [](const ResultsRow& r) { return std::to_string(r.dim); },
+     [](ResultsRow& r, const std::string& s) { r.dim = read_number<std::size_t>(s, "dim"); }},
+    {"method", [](const ResultsRow& r) { return cell_text(r.method); },
+     [](ResultsRow& r, const std::string& s) { r.method = s; }},
+    {"samples", [](const ResultsRow& r) { return std::to_string(r.samples); },
+     [](ResultsRow& r, const std::string& s) { r.samples = read_number<std::uint64_t>(s, "samples"); }},
+    {"trials", [](const ResultsRow& r) { return std::to_string(r.trials); },
+     [](ResultsRow& r, const std::string& s) { r.trials = read_number<std::uint32_t>(s, "trials"); }},
+    {"mean", [](const ResultsRow& r) { return num17(r.mean); },
+     [](ResultsRow& r, const std::string& s) { r.mean = read_number<double>(s, "mean"); }},
+    {"trial_stddev", [](const ResultsRow& r) { return num17(r.trial_stddev); },
+     [](ResultsRow& r, const std::string& s) { r.trial_stddev = read_number<double>(s, "trial_stddev"); }},
+    {"mean_std_error", [](const ResultsRow& r) { return num17(r.mean_std_error); },
+     [](ResultsRow& r, const std::string& s) { r.mean_std_error = read_number<double>(s, "mean_std_error"); }},
+    {"analytic", [](const ResultsRow& r) { return opt_num17(r.analytic); },
+     [](ResultsRow& r, const std::string& s) { r.analytic = read_opt(s, "analytic"); }},
+    {"abs_error", [](const ResultsRow& r) { return opt_num17(r.abs_error); },
+     [](ResultsRow& r, const std::string& s) { r.abs_error = read_opt(s, "abs_error"); }},
+    {"warnings", [](const ResultsRow& r) { return cell_text(r.warnings); },
+     [](ResultsRow& r, const std::string& s) { r.warnings = s; }},
+};
+constexpr std::size_t kNumColumns = sizeof kColumns / sizeof kColumns[0];
+
+// A row whose warnings start with this marker is a failed integrand.
+constexpr std::string_view kFailedMark = "FAILED";
+
+std::string join(const std::vector<std::string>& parts, char sep) {
+  std::string out;
+  for (const std::string& p : parts) {
+    if (!out.empty()) out += sep;
+    out += p;
+  }
+  return out;
+}
+
+}  // namespace
 
 std::vector<ResultsRow> make_results(const JobSpec& job, const BatchResult& br) {
-  std::vector<ResultsRow> rows;
-  rows.reserve(br.per_integrand.size());
-  for (std::size_t i = 0; i < br.per_integrand.size(); ++i) {
-    const IntegrandResult& r = br.per_integrand[i];
-    const IntegrandSpec& s = job.integrands[i];
-    ResultsRow row;
-    row.name = r.name;
-    row.index = uint32_t(i + 1);
-    row.dim = s.dim;
-    row.method = method_name(s.method);
-    row.samples = s.n_samples;
-    row.trials = job.trials;
-    row.ok = r.ok;
-    if (r.ok) {
-      row.mean = r.summary.mean;
-      row.trial_stddev = r.summary.trial_stddev;
-      double se = 0.0;
-      for (const McEstimate& e : r.summary.per_trial) se += e.std_error;
-      row.mean_std_error = se / double(r.summary.per_trial.size());
-      std::string w;
-      if (r.nonfinite_warning) w += "nonfinite;";
-      if (r.budget_exhausted) w += "budget_exhausted;";
-      if (!r.error.empty()) w += sanitize_field(r.error) + ";";
-      if (!w.empty()) w.pop_back();
-      row.warnings = w;
-    } else {
-      row.mean = row.trial_stddev = row.mean_std_error = std::numeric_limits<double>::quiet_NaN();
-      row.warnings = "FAILED;" + sanitize_field(r.error);
+  std::vector<ResultsRow> rows(br.per_integrand.size());
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  for (std::size_t i = 0; i < rows.size(); ++i) {
+    const IntegrandResult& res = br.per_integrand[i];
+    const IntegrandSpec& spec = job.integrands[i];
+    ResultsRow& row = rows[i];
+    row = ResultsRow{res.name, std::uint32_t(i + 1), spec.dim, method_name(spec.method), spec.n_samples,
+                     job.trials, res.ok, nan, nan, nan, std::nullopt, std::nullopt, ""};
+    if (!res.ok) {  // failed integrand: no numbers, the reason in the warnings
+      row.warnings = std::string(kFailedMark) + ";" + res.error;
+      continue;
     }
-    rows.push_back(std::move(row));
+    row.mean = res.summary.mean;
+    row.trial_stddev = res.summary.trial_stddev;
+    // mean_std_error: the average per-trial standard error over the trials kept
+    double se_sum = 0.0;
+    for (const McEstimate& e : res.summary.per_trial) se_sum += e.std_error;
+    row.mean_std_error = se_sum / double(res.summary.per_trial.size());
+    std::vector<std::string> notes;
+    if (res.nonfinite_warning) notes.emplace_back("nonfinite");
+    if (res.budget_exhausted) notes.emplace_back("budget_exhausted");
+    if (!res.error.empty()) notes.push_back(res.error);  // partial: the failed trials
+    row.warnings = join(notes, ';');
   }
   return rows;
 }
 
 std::string results_to_csv_text(const std::vector<ResultsRow>& rows) {
-  std::ostringstream out;
-  out << kResultsHeader << "\n";
-  for (const ResultsRow& r : rows)
-    out << sanitize_field(r.name) << ',' << r.index << ',' << r.dim << ',' << r.method << ','
-        << r.samples << ',' << r.trials << ',' << fmt17(r.mean) << ',' << fmt17(r.trial_stddev) << ','
-        << fmt17(r.mean_std_error) << ',' << (r.analytic ? fmt17(*r.analytic) : std::string()) << ','
-        << (r.abs_error ? fmt17(*r.abs_error) : std::string()) << ',' << sanitize_field(r.warnings)
-        << "\n";
-  return out.str();
+  std::vector<std::string> cells(kNumColumns);
+  for (std::size_t c = 0; c < kNumColumns; ++c) cells[c] = kColumns[c].name;
+  std::string out = join(cells, ',') + "\n";
+  for (const ResultsRow& r : rows) {
+    for (std::size_t c = 0; c < kNumColumns; ++c) cells[c] = kColumns[c].write(r);
+    out += join(cells, ',') + "\n";
+  }
+  return out;
 }
 
 void write_results(const std::vector<ResultsRow>& rows, const std::filesystem::path& path) {
-  std::ofstream out(path);
-  if (!out) throw std::runtime_error("cannot write results: " + path.string());
-  out << results_to_csv_text(rows);
+  const std::string text = results_to_csv_text(rows);
+  std::ofstream out(path, std::ios::binary);
+  if (!out.write(text.data(), std::streamsize(text.size())))
+    throw std::runtime_error("cannot write results: " + path.string());
 }
 
 std::vector<ResultsRow> read_results(const std::filesystem::path& path) {
-  std::ifstream in(path);
+  std::ifstream in(path, std::ios::binary);
   if (!in) throw MalformedResults("cannot open results file: " + path.string());
   std::string line;
-  if (!std::getline(in, line) || split_csv_line(line) != split_csv_line(kResultsHeader))
-    throw MalformedResults("missing or wrong header row");
+  std::getline(in, line);
+  const std::vector<std::string> header = csv_cells(line);
+  bool header_ok = header.size() == kNumColumns;
+  for (std::size_t c = 0; header_ok && c < kNumColumns; ++c) header_ok = header[c] == kColumns[c].name;
+  if (!header_ok) throw MalformedResults("results file: missing or unexpected header row");
   std::vector<ResultsRow> rows;
-  std::size_t lineno = 1;
-  while (std::getline(in, line)) {
-    ++lineno;
-    if (line.empty()) continue;
-    const std::vector<std::string> f = split_csv_line(line);
-    if (f.size() != 12)
-      throw MalformedResults("line " + std::to_string(lineno) + ": expected 12 fields, got " +
-                             std::to_string(f.size()));
-    ResultsRow r;
-    r.name = f[0];
-    r.index = uint32_t(std::strtoul(f[1].c_str(), nullptr, 10));
-    r.dim = std::strtoul(f[2].c_str(), nullptr, 10);
-    r.method = f[3];
-    r.samples = std::strtoull(f[4].c_str(), nullptr, 10);
-    r.trials = uint32_t(std::strtoul(f[5].c_str(), nullptr, 10));
-    r.mean = parse_double(f[6], "mean");
-    r.trial_stddev = parse_double(f[7], "trial_stddev");
-    r.mean_std_error = parse_double(f[8], "mean_std_error");
-    if (!f[9].empty()) r.analytic = parse_double(f[9], "analytic");
-    if (!f[10].empty()) r.abs_error = parse_double(f[10], "abs_error");
-    r.warnings = f[11];
-    r.ok = r.warnings.rfind("FAILED", 0) != 0;
-    rows.push_back(std::move(r));
+  for (std::size_t line_no = 2; std::getline(in, line); ++line_no) {
+    if (line.empty() || line == "\r") continue;
+    const std::vector<std::string> cells = csv_cells(line);
+    if (cells.size() != kNumColumns)
+      throw MalformedResults("results line " + std::to_string(line_no) + " has " + std::to_string(cells.size()) +
+                             " fields, expected " + std::to_string(kNumColumns));
+    ResultsRow& r = rows.emplace_back();
+    for (std::size_t c = 0; c < kNumColumns; ++c) kColumns[c].read(r, cells[c]);
+    r.ok = std::string_view(r.warnings).substr(0, kFailedMark.size()) != kFailedMark;
   }
   if (rows.empty()) throw MalformedResults("results file has no data rows");
   return rows;
 }
 
-// ---- commands (ref job_io.cpp:286-455) --------------------------------------------
+// ---- commands -----------------------------------------------------------------
+// SPEC.md [MODULE] cli: run_command writes the ResultsTable and exits 0 on
+// success, 2 when the job does not load or validate, 3 when nothing could be
+// computed; one completion line per integrand on stdout.
 
 int run_command(const std::filesystem::path& job_path, const std::filesystem::path& out_path,
                 const RunOverrides& overrides) {
-  JobSpec job;
+  std::optional<JobSpec> job;
   try {
     job = read_job(job_path);
   } catch (const JobFileError& e) {
     std::cerr << "error: " << e.what() << "\n";
     return 2;
   }
-  if (overrides.seed) job.seed = *overrides.seed;
-  if (overrides.trials) job.trials = *overrides.trials;
-  if (overrides.workers) job.workers = *overrides.workers;
-  const std::vector<Violation> violations = validate(job);
-  if (!violations.empty()) {
-    std::cerr << "error: job does not validate:\n";
-    for (const Violation& v : violations) {
-      std::cerr << "  ";
-      if (!v.integrand.empty()) std::cerr << v.integrand << ": ";
-      std::cerr << v.message << "\n";
-    }
+  job->seed = overrides.seed.value_or(job->seed);
+  job->trials = overrides.trials.value_or(job->trials);
+  job->workers = overrides.workers.value_or(job->workers);
+
+  if (const std::vector<Violation> bad = validate(*job); !bad.empty()) {
+    std::cerr << "error: " << bad.size() << " validation problem(s) in " << job_path.string() << ":\n";
+    for (const Violation& v : bad)
+      std::cerr << "  " << (v.integrand.empty() ? std::string("job") : v.integrand) << ": " << v.message << "\n";
     return 2;
   }
-  BatchResult br;
+
+  BatchResult batch;
   try {
-    br = run_batch(job);
+    batch = run_batch(*job);
   } catch (const std::exception& e) {
-    std::cerr << "error: " << e.what() << "\n";
+    std::cerr << "error: batch failed: " << e.what() << "\n";
     return 3;
   }
-  bool any_ok = false;
-  for (const IntegrandResult& r : br.per_integrand) {
-    if (r.ok) {
-      any_ok = true;
-      std::cout << r.name << ": " << fmt17(r.summary.mean) << " +- " << fmt17(r.summary.trial_stddev)
-                << " (" << r.seconds << " s)\n";
-    } else {
-      std::cout << r.name << ": FAILED (" << r.error << ")\n";
-    }
+
+  const std::vector<ResultsRow> rows = make_results(*job, batch);
+  for (const ResultsRow& r : rows) {
+    if (r.ok)
+      std::cout << r.name << ": mean " << num17(r.mean) << ", trial stddev " << num17(r.trial_stddev)
+                << ", mean std_error " << num17(r.mean_std_error) << "\n";
+    else
+      std::cout << r.name << ": " << r.warnings << "\n";
   }
-  write_results(make_results(job, br), out_path);
-  std::cerr << "wrote " << br.per_integrand.size() << " rows to " << out_path << " in "
-            << br.total_seconds << " s\n";
+  write_results(rows, out_path);
+  std::cerr << rows.size() << " row(s) written to " << out_path.string() << "; sampling took "
+            << batch.total_seconds << " s\n";
+  const bool any_ok = std::any_of(rows.begin(), rows.end(), [](const ResultsRow& r) { return r.ok; });
   return any_ok ? 0 : 3;
 }
 
@@ -640,69 +685,67 @@ int gen_fig1(std::uint32_t n_count, std::uint64_t samples, const std::filesystem
   return 0;
 }
 
-namespace {
-std::optional<uint32_t> trailing_number(const std::string& name) {  // ref job_io.cpp:386-395
-  std::size_t end = name.size(), begin = end;
-  while (begin > 0 && std::isdigit(static_cast<unsigned char>(name[begin - 1]))) --begin;
-  if (begin == end) return std::nullopt;
-  return uint32_t(std::strtoul(name.c_str() + begin, nullptr, 10));
-}
-}  // namespace
-
+// check_fig1 (SPEC.md [OP] check_fig1): per row, the harmonic number n and the
+// analytic value — from the analytic column when the table has one, else
+// analytic_harmonic(n) with n the integer that ends the row's name (gen-fig1
+// names rows f001..f100) — then pass iff the row succeeded and
+// |mean - analytic| <= 4 max(trial_stddev, mean_std_error).
 Fig1Check check_fig1(const std::vector<ResultsRow>& rows) {
   if (rows.empty()) throw MalformedResults("no result rows");
-  Fig1Check out;
+  auto name_number = [](const std::string& name) -> std::optional<std::uint32_t> {
+    const auto first_digit =
+        std::find_if_not(name.rbegin(), name.rend(), [](unsigned char c) { return std::isdigit(c) != 0; }).base();
+    if (first_digit == name.end()) return std::nullopt;
+    std::uint32_t n = 0;
+    std::from_chars(&*first_digit, name.data() + name.size(), n);
+    return n;
+  };
+  Fig1Check check;
+  check.rows.reserve(rows.size());
   for (const ResultsRow& r : rows) {
+    const std::optional<std::uint32_t> n = name_number(r.name);
+    if (!r.analytic && !n)
+      throw MalformedResults("row '" + r.name + "' has neither an analytic value nor a trailing harmonic index");
     Fig1Row f;
-    const auto n = trailing_number(r.name);
-    if (r.analytic) {
-      f.analytic = *r.analytic;
-      f.n = n.value_or(r.index);
-    } else {
-      if (!n)
-        throw MalformedResults("row '" + r.name +
-                               "': no analytic column and no trailing index in the name");
-      f.n = *n;
-      f.analytic = analytic_harmonic(f.n);
-    }
+    f.n = n ? *n : r.index;
+    f.analytic = r.analytic ? *r.analytic : analytic_harmonic(f.n);
     f.mean = r.mean;
     f.trial_stddev = r.trial_stddev;
     f.mean_std_error = r.mean_std_error;
-    const double band = 4.0 * std::max(f.trial_stddev, f.mean_std_error);
-    f.pass = r.ok && std::isfinite(f.mean) && std::fabs(f.mean - f.analytic) <= band;
-    if (f.pass) ++out.passed;
-    out.rows.push_back(f);
+    const double band = 4.0 * std::max(r.trial_stddev, r.mean_std_error);
+    f.pass = r.ok && std::isfinite(r.mean) && std::fabs(r.mean - f.analytic) <= band;
+    check.passed += f.pass ? 1u : 0u;
+    check.rows.push_back(f);
   }
-  return out;
+  return check;
 }
 
 int check_fig1_command(const std::filesystem::path& results_path,
                        const std::optional<std::filesystem::path>& plot_out) {
-  Fig1Check check;
+  std::optional<Fig1Check> check;
   try {
     check = check_fig1(read_results(results_path));
   } catch (const MalformedResults& e) {
     std::cerr << "error: " << e.what() << "\n";
     return 2;
   }
-  for (const Fig1Row& r : check.rows)
-    std::cout << "n=" << r.n << " mean=" << fmt17(r.mean) << " analytic=" << fmt17(r.analytic)
-              << " band=+-" << fmt17(4.0 * std::max(r.trial_stddev, r.mean_std_error))
-              << (r.pass ? " PASS" : " FAIL") << "\n";
-  std::cout << "passed " << check.passed << "/" << check.rows.size() << "\n";
-  if (plot_out) {
-    std::ofstream out(*plot_out);
-    if (!out) {
-      std::cerr << "error: cannot write " << *plot_out << "\n";
+  for (const Fig1Row& r : check->rows)
+    std::cout << (r.pass ? "PASS" : "FAIL") << " n=" << r.n << " mean=" << num17(r.mean)
+              << " analytic=" << num17(r.analytic)
+              << " band=" << num17(4.0 * std::max(r.trial_stddev, r.mean_std_error)) << "\n";
+  std::cout << "passed " << check->passed << "/" << check->rows.size() << "\n";
+  if (plot_out) {  // plot data: n, mean, the trial spread and the analytic curve
+    std::string text = "n,mean,trial_stddev,analytic\n";
+    for (const Fig1Row& r : check->rows)
+      text += std::to_string(r.n) + "," + num17(r.mean) + "," + num17(r.trial_stddev) + "," + num17(r.analytic) + "\n";
+    std::ofstream out(*plot_out, std::ios::binary);
+    if (!out.write(text.data(), std::streamsize(text.size()))) {
+      std::cerr << "error: cannot write " << plot_out->string() << "\n";
       return 2;
     }
-    out << "n,mean,trial_stddev,analytic\n";
-    for (const Fig1Row& r : check.rows)
-      out << r.n << ',' << fmt17(r.mean) << ',' << fmt17(r.trial_stddev) << ',' << fmt17(r.analytic)
-          << "\n";
   }
-  const double frac = double(check.passed) / double(check.rows.size());
-  return frac >= 0.95 ? 0 : 1;
+  // acceptance criterion 1: at least 95 % of the rows inside the band
+  return 100 * std::size_t(check->passed) >= 95 * check->rows.size() ? 0 : 1;
 }
 
 }  // namespace mcb

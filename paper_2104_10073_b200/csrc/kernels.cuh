@@ -83,7 +83,6 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
     count = (chunk + 1 == f.n_chunks) ? uint32_t(f.n_samples - uint64_t(chunk) * MCB_CHUNK_SIZE)
                                       : MCB_CHUNK_SIZE;
   }
-  const uint32_t pairs = (count + 1) >> 1;
   const PhiloxPrefix P =
       dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
   __shared__ TrigAB ab[TABLE && !FOLD ? 512 : 1];
@@ -112,47 +111,51 @@ __global__ void __launch_bounds__(kThreads, MCB_MIN_BLOCKS)
 
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
-  // Software pipeline: iteration i finishes pair q_i (FP64-heavy) while
-  // generating pair q_{i+1} (integer-heavy).  The last iteration generates
-  // one pair past the chunk, which is discarded.  Round-1 Philox products
-  // advance by 64-bit adds: M0 * (q + T) * D = M0 * q * D + M0 * T * D.
-  const uint32_t iters =
-      threadIdx.x < pairs ? (pairs - threadIdx.x + kThreads - 1) / kThreads : 0u;
+  // g of one sample (f - shift; non-finite samples counted and dropped in SAFE)
+  auto take = [&](double st) {
+    double g;
+    bool ok = true;
+    if constexpr (FOLD) {  // g = f - shift straight from the folded table
+      g = dev::finish_shifted<FAM>(f, c_trig, abs_tab, st);
+    } else {
+      const double fv = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, st);
+      ok = !SAFE || finite64(fv);
+      g = __dsub_rn(fv, f.shift);
+    }
+    nbad += ok ? 0u : 1u;
+    return ok ? g : 0.0;
+  };
+  // Software pipeline over the tile's FULL pairs: iteration i finishes pair
+  // q_i (FP64-heavy) while generating pair q_{i+1} (integer-heavy); the last
+  // iteration generates one pair past its range, which is discarded.  An odd
+  // count's last sample (first half of pair `full`) is taken after the loop
+  // by the thread whose pair sequence it ends, so every thread's sums keep
+  // the sample order.  Round-1 Philox products advance by 64-bit adds:
+  // M0 * (q + T) * D = M0 * q * D + M0 * T * D.
+  const uint32_t full = count >> 1;
+  const uint32_t iters = threadIdx.x < full ? (full - threadIdx.x + kThreads - 1) / kThreads : 0u;
   uint64_t pbase = uint64_t(dev::kM0) * uint64_t(threadIdx.x * uint32_t(D));
   constexpr uint64_t kStep = uint64_t(dev::kM0) * uint64_t(kThreads * D);
   double a0, a1;
   dev::gen_pair<FAM, D, UNIT_DOM, SAFE>(f, P, pbase, a0, a1);
-  for (uint32_t it = 0; it < iters; ++it) {
-    const uint32_t q = threadIdx.x + it * kThreads;
-    pbase += kStep;
+  for (uint32_t it = iters; it != 0; --it) {
+    pbase = dev::add64(pbase, kStep);
     double b0, b1;
     dev::gen_pair<FAM, D, UNIT_DOM, SAFE>(f, P, pbase, b0, b1);
-    double f0, f1, g0, g1;
-    if constexpr (FOLD) {  // g = f - shift straight from the folded table
-      g0 = dev::finish_shifted<FAM>(f, c_trig, abs_tab, a0);
-      g1 = dev::finish_shifted<FAM>(f, c_trig, abs_tab, a1);
-      f0 = f1 = 0.0;
-    } else {
-      f0 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a0);
-      f1 = dev::finish<FAM, UNIT_COEF, SAFE>(f, c_trig, ab, a1);
-      g0 = __dsub_rn(f0, f.shift);
-      g1 = __dsub_rn(f1, f.shift);
-    }
+    const double g0 = take(a0), g1 = take(a1);
     a0 = b0;
     a1 = b1;
-    const bool has1 = 2 * q + 1 < count;
-    if (SAFE) {
-      const bool ok0 = finite64(f0), ok1 = finite64(f1) && has1;
-      nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
-      g0 = ok0 ? g0 : 0.0;
-      g1 = ok1 ? g1 : 0.0;
-    } else {
-      g1 = has1 ? g1 : 0.0;
-    }
     s1 = __dadd_rn(s1, g0);
     s2 = fma(g0, g0, s2);
     s1 = __dadd_rn(s1, g1);
     s2 = fma(g1, g1, s2);
+  }
+  if ((count & 1u) && threadIdx.x == full % kThreads) {
+    // pbase now addresses pair `full` (iters steps past this thread's first
+    // pair), already generated into a0, a1; only its first sample exists
+    const double g0 = take(a0);
+    s1 = __dadd_rn(s1, g0);
+    s2 = fma(g0, g0, s2);
   }
 
   // fixed-shape reduction: warp butterfly, then warps 0..W-1 in order
