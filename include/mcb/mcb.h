@@ -215,6 +215,15 @@ MCB_API mcb_status mcb_program_info(const mcb_program* program, uint32_t* n_inst
 MCB_API size_t mcb_program_param_name(const mcb_program* program, uint32_t i, char* buf,
                                       size_t cap);
 
+/* CompiledProgram::evaluate (ref/src/expr.cpp:520-553) of `program` at
+ * caller-given points, on the GPU interpreter the estimators use: `n_points`
+ * rows of the program's dim coordinates (row-major), `params` in binding
+ * (sorted-name) order, n_params = the program's parameter count.
+ * Non-finite values are returned as they are.  Synchronous. */
+MCB_API mcb_status mcb_program_eval_points(const mcb_program* program, const double* params,
+                                           size_t n_params, const double* points, uint64_t n_points,
+                                           int device, double* out);
+
 /* ---- the hot path -------------------------------------------------------- */
 /* run_batch (src/batch.cpp:195-333): every integrand, every trial t in
  * [0, trials), StreamKey {seed, integrand_index, t, chunk}, by each

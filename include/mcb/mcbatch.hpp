@@ -24,6 +24,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mcb/mcb.h"
@@ -256,6 +257,10 @@ struct CompiledSource {
   CompiledSource(const CompiledSource&) = delete;
   CompiledSource& operator=(const CompiledSource&) = delete;
   CompiledSource(CompiledSource&& o) noexcept : handle(o.handle) { o.handle = nullptr; }
+  CompiledSource& operator=(CompiledSource&& o) noexcept {
+    std::swap(handle, o.handle);
+    return *this;
+  }
   ~CompiledSource() { mcb_program_destroy(handle); }
 };
 // Throws std::invalid_argument with the reference's validation wording.

@@ -256,6 +256,52 @@ int ref_run_harmonic(std::uint32_t n_total, std::uint64_t samples, std::uint32_t
   }
 }
 
+// Expression front-end dump (parity of include/mcbatch/expr.hpp): for
+// `source` compiled for `dim` coordinates and the comma-separated parameter
+// names, one line "OK <stack_need> <postfix> <tree_eval hex> <to_string>" or
+// "ERR <error class>".  Postfix: op:index:value-hex per instruction.
+// The same format is printed by tests/cpp/test_compat.cpp for our layer.
+int ref_expr_dump(const char* source, std::uint32_t dim, const char* names_csv, const double* point,
+                  const double* params, char* out, std::size_t cap) {
+  std::string line;
+  std::vector<std::string> names;
+  for (std::string cur, all = names_csv; !all.empty();) {
+    std::size_t c = all.find(',');
+    names.push_back(all.substr(0, c));
+    all = c == std::string::npos ? "" : all.substr(c + 1);
+  }
+  auto hex = [](double v) {
+    std::uint64_t u;
+    std::memcpy(&u, &v, 8);
+    char b[24];
+    std::snprintf(b, sizeof b, "%016llx", (unsigned long long)u);
+    return std::string(b);
+  };
+  try {
+    Expr e = parse(source);
+    CompiledProgram p = compile(e, dim, names);
+    line = "OK " + std::to_string(p.stack_need()) + " ";
+    for (const Instr& in : p.code())
+      line += std::to_string(int(in.op)) + ":" + std::to_string(in.index) + ":" + hex(in.value) + ",";
+    line += " " + hex(tree_eval(e, {point, dim}, names, {params, names.size()}));
+    line += " " + std::to_string(parse(to_string(e)) == e);
+  } catch (const SyntaxError&) {
+    line = "ERR SyntaxError";
+  } catch (const UnknownFunction&) {
+    line = "ERR UnknownFunction";
+  } catch (const ArityMismatch&) {
+    line = "ERR ArityMismatch";
+  } catch (const DimensionError&) {
+    line = "ERR DimensionError";
+  } catch (const UnboundParameter&) {
+    line = "ERR UnboundParameter";
+  } catch (const std::exception& ex) {
+    line = std::string("ERR other");
+  }
+  std::snprintf(out, cap, "%s", line.c_str());
+  return int(line.size());
+}
+
 // evaluate (src/expr.cpp:520-553) of an arbitrary source with named params.
 int ref_eval_source(const char* source, std::uint32_t dim, const char* const* names,
                     const double* values, std::size_t n_params, const double* pts,

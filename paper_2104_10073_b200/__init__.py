@@ -109,6 +109,7 @@ ABI_SYMBOLS = [
     "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
     "mcb_program_param_name", "mcb_stratified_plan", "mcb_tree_refine", "mcb_program_jit",
     "mcb_program_jit_compiles", "mcb_program_jit_error", "mcb_program_jit_build", "mcb_stratified_mc",
+    "mcb_program_eval_points",
 ]
 
 
@@ -143,6 +144,7 @@ def _load() -> ctypes.CDLL:
         "mcb_probe_philox_peak": (i32, [i32, dbl, P(dbl)]),
         "mcb_program_compile": (i32, [ctypes.c_char_p, u32, P(ctypes.c_char_p), sz, P(vp)]),
         "mcb_program_destroy": (None, [vp]),
+        "mcb_program_eval_points": (i32, [vp, P(ctypes.c_double), sz, vp, u64, i32, vp]),
         "mcb_program_info": (i32, [vp, P(u32), P(u32), P(u32)]),
         "mcb_program_param_name": (sz, [vp, u32, ctypes.c_char_p, sz]),
         "mcb_stratified_plan": (i32, [P(Integrand), P(u32), P(u64), P(u32)]),
@@ -238,7 +240,22 @@ class Program:
                            low=low, high=high, n_samples=n_samples, index=index)
         f.program = self._h.value
         f.a = f.b = 0.0
+        f._program_ref = self  # the descriptor holds the raw handle: keep the program alive
         return f
+
+    def evaluate(self, points, params: Optional[Dict[str, float]] = None, device: int = 0) -> np.ndarray:
+        """CompiledProgram::evaluate (ref src/expr.cpp:520-553) at the given
+        points ((n, dim) array) on the GPU interpreter the estimators use."""
+        params = params or {}
+        missing = [n for n in self.param_names if n not in params]
+        if missing:
+            raise ValueError(f"unbound parameter '{missing[0]}'")
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, self.dim)
+        pv = (ctypes.c_double * max(1, len(self.param_names)))(*[params[n] for n in self.param_names])
+        out = np.zeros(len(pts))
+        _check(lib.mcb_program_eval_points(self._h, pv, len(self.param_names), pts.ctypes.data, len(pts), device,
+                                           out.ctypes.data))
+        return out
 
     def jit_build(self) -> None:
         """NVRTC-compile this program's specialised kernels now (no device needed)."""
@@ -276,6 +293,9 @@ def as_array(fns: Sequence[Integrand]):
     arr = (Integrand * len(fns))()
     for i, f in enumerate(fns):
         arr[i] = f
+    # programs referenced by raw handle stay alive as long as the array
+    arr._programs = [p for p in {id(p): p for p in (getattr(f, "_program_ref", None) for f in fns)}.values()
+                     if p is not None]
     return arr
 
 
@@ -367,7 +387,19 @@ def parameter_scan(program: "Program", params: Dict[str, float], name: str, valu
     fns = [program.integrand({**params, name: float(v)}, low=low, high=high, n_samples=n_samples, index=i)
            for i, v in enumerate(values)]
     out = run_direct(fns, seed, trials, devices)
-    return out, [summarize_trials(row) for row in out]
+    # the reference's success rule (src/batch.cpp:320-329): with two or more
+    # trials an integrand needs at least two successful ones, else one; a
+    # failed integrand makes the scan throw (src/batch.cpp:360-364)
+    need = 2 if trials >= 2 else 1
+    summaries = []
+    for i, row in enumerate(out):
+        n_ok = int((row["status"] == TRIAL_OK).sum())
+        if n_ok < need:
+            bad = [f"trial {t}: status {int(row[t]['status'])}" for t in range(trials) if row[t]["status"] != TRIAL_OK]
+            raise RuntimeError(f"parameter_scan: {name}#{i} failed: {n_ok} of {trials} trials succeeded "
+                               f"({'; '.join(bad)})")
+        summaries.append(summarize_trials(row))
+    return out, summaries
 
 
 def direct_mc(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, device: int = 0):

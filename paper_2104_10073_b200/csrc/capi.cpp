@@ -609,6 +609,54 @@ mcb_status mcb_debug_eval(const mcb_integrand* fn, uint64_t seed, uint32_t trial
   return MCB_OK;
 }
 
+mcb_status mcb_program_eval_points(const mcb_program* program, const double* params, size_t n_params,
+                                   const double* points, uint64_t n_points, int device, double* out) {
+  if (!program || (n_points && (!points || !out)) || (n_params && !params))
+    return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (n_params != program->p.param_names.size())
+    return fail(MCB_ERR_INVALID_ARGUMENT, "program binds " + std::to_string(program->p.param_names.size()) +
+                                              " parameter(s), got " + std::to_string(n_params));
+  mcb_status st = check_device(device);
+  if (st != MCB_OK) return st;
+  if (n_points == 0) return MCB_OK;
+  DeviceGuard guard(device);
+  FnDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.dim = program->p.dim;
+  d.prog_len = uint32_t(program->p.code.size());
+  d.n_consts = uint32_t(program->p.consts.size());
+  for (size_t i = 0; i < n_params; ++i) d.k[i] = params[i];
+  const auto& w = program->words;
+  const auto& c = program->p.consts;
+  const size_t n_coord = size_t(n_points) * program->p.dim;
+  FnDesc* d_fn = nullptr;
+  uint32_t* d_code = nullptr;
+  double *d_consts = nullptr, *d_pts = nullptr, *d_out = nullptr;
+  cudaError_t e = cudaMalloc(&d_fn, sizeof(FnDesc));
+  if (e == cudaSuccess) e = cudaMalloc(&d_code, sizeof(uint32_t) * std::max<size_t>(w.size(), 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_consts, sizeof(double) * std::max<size_t>(c.size(), 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_pts, sizeof(double) * std::max<size_t>(n_coord, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, sizeof(double) * n_points);
+  if (e == cudaSuccess) e = cudaMemcpy(d_fn, &d, sizeof d, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !w.empty())
+    e = cudaMemcpy(d_code, w.data(), sizeof(uint32_t) * w.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !c.empty())
+    e = cudaMemcpy(d_consts, c.data(), sizeof(double) * c.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && n_coord)
+    e = cudaMemcpy(d_pts, points, sizeof(double) * n_coord, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = mcb::detail::launch_program_points(int(program->p.dim), d_fn, d_code, d_consts, program->p.depth,
+                                           d_pts, n_points, d_out, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(out, d_out, sizeof(double) * n_points, cudaMemcpyDeviceToHost);
+  cudaFree(d_fn);
+  cudaFree(d_code);
+  cudaFree(d_consts);
+  cudaFree(d_pts);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_fail(e, "program_eval_points");
+  return MCB_OK;
+}
+
 int mcb_program_jit(int mode) {
   if (mode >= 0) mcb::jit::set_mode(mode);
   return mcb::jit::mode();

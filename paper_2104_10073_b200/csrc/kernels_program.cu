@@ -395,6 +395,30 @@ __global__ void __launch_bounds__(T) k_program_eval(const FnDesc* __restrict__ f
   }
 }
 
+// CompiledProgram::evaluate at caller-given points (mcb_program_eval_points):
+// the interpreter above on coordinates read from global memory, two points
+// per thread as in the sampling kernels.  No sampler, no reduction.
+template <int D>
+__global__ void __launch_bounds__(T) k_program_points(const FnDesc* __restrict__ fn,
+                                                      const uint32_t* __restrict__ code,
+                                                      const double* __restrict__ consts, uint32_t slots,
+                                                      const double* __restrict__ pts, uint64_t n,
+                                                      double* __restrict__ out) {
+  const FnDesc f = *fn;
+  __shared__ double params[prog::kMaxParams];
+  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  const uint64_t first = 2 * (uint64_t(blockIdx.x) * T + threadIdx.x);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      m.X[(j * 2 + h) * T + threadIdx.x] = first + h < n ? pts[(first + h) * D + j] : 0.0;
+  interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (first + h < n) out[first + h] = m.S[h * T + threadIdx.x];
+}
+
 // ---- dispatch ------------------------------------------------------------------
 
 using ProgFn = void (*)(const FnDesc*, const uint32_t*, uint64_t, TilePartial*, const uint32_t*,
@@ -501,6 +525,34 @@ cudaError_t launch_program_eval(int dim, int variant, const FnDesc* fn, const ui
   e->eval<<<(n_pairs + T - 1) / T, T, program_smem_bytes(slots, dim), s>>>(
       fn, code, consts, slots, trial, chunk, first_pair, n_pairs, out);
   return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t program_points_d(const FnDesc* fn, const uint32_t* code, const double* consts,
+                                    uint32_t slots, const double* pts, uint64_t n, double* out, cudaStream_t s) {
+  const size_t smem = program_smem_bytes(slots, D);
+  cudaError_t e = cudaFuncSetAttribute(k_program_points<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const uint64_t pairs = (n + 1) / 2;
+  k_program_points<D><<<dim3(uint32_t((pairs + T - 1) / T)), dim3(T), smem, s>>>(fn, code, consts, slots, pts, n,
+                                                                                 out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_program_points(int dim, const FnDesc* fn, const uint32_t* code, const double* consts,
+                                  uint32_t slots, const double* pts, uint64_t n, double* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  switch (dim) {
+    case 1: return program_points_d<1>(fn, code, consts, slots, pts, n, out, s);
+    case 2: return program_points_d<2>(fn, code, consts, slots, pts, n, out, s);
+    case 3: return program_points_d<3>(fn, code, consts, slots, pts, n, out, s);
+    case 4: return program_points_d<4>(fn, code, consts, slots, pts, n, out, s);
+    case 5: return program_points_d<5>(fn, code, consts, slots, pts, n, out, s);
+    case 6: return program_points_d<6>(fn, code, consts, slots, pts, n, out, s);
+    case 7: return program_points_d<7>(fn, code, consts, slots, pts, n, out, s);
+    case 8: return program_points_d<8>(fn, code, consts, slots, pts, n, out, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace detail

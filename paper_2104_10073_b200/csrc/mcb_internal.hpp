@@ -116,6 +116,9 @@ cudaError_t launch_program_group(const GroupLaunch& g, const dev::FnDesc* fns,
 cudaError_t launch_program_eval(int dim, int variant, const dev::FnDesc* fn, const uint32_t* code,
                                 const double* consts, uint32_t slots, uint32_t trial, uint32_t chunk,
                                 uint32_t first_pair, uint32_t n_pairs, double* out, cudaStream_t s);
+cudaError_t launch_program_points(int dim, const dev::FnDesc* fn, const uint32_t* code,
+                                  const double* consts, uint32_t slots, const double* pts, uint64_t n,
+                                  double* out, cudaStream_t s);
 cudaError_t launch_philox_probe(const uint32_t* key, uint32_t* sink, int n_ctas, int iters,
                                cudaStream_t s);
 

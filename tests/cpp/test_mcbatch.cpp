@@ -436,6 +436,46 @@ static void stratified_cases() {
   CHECK_THROWS_AS(stratified_mc(f, 10, 10, StreamKey{3, 0, 0, 0}, 50), CellBudgetExceeded);
 }
 
+// src/batch.cpp:302-331: trials that fail are dropped; the integrand is ok
+// ("partial: trial t: ...") with at least two successful trials when trials
+// >= 2, else failed.  One stratified cell of 2 samples of sqrt(x1 - 0.5) on
+// [0,1]: a trial whose two points (cell 0 = chunk key 0, StreamKey {seed, 0,
+// t, 0}, points 0 and 1 — checked independently with sample_uniform) both lie
+// below 0.5 has a dead cell and fails.
+static void partial_trials() {
+  for (std::uint32_t trials : {12u, 3u}) {
+    IntegrandSpec s = IntegrandSpec::from_source("half", "sqrt(x1 - 0.5)", 1, HyperRect::unit(1), {}, 2);
+    s.method = Method::Stratified;
+    RefineConfig rc;
+    rc.init_cells_per_dim = 1;
+    s.method_config = rc;
+    for (std::uint64_t seed = 1; seed < 40; ++seed) {
+      JobSpec job;
+      job.seed = seed;
+      job.trials = trials;
+      job.integrands = {s};
+      std::vector<std::uint32_t> dead;
+      for (std::uint32_t t = 0; t < trials; ++t) {
+        const std::vector<double> x = sample_uniform(HyperRect::unit(1), StreamKey{seed, 0, t, 0}, 2);
+        if (x[0] < 0.5 && x[1] < 0.5) dead.push_back(t);
+      }
+      if (dead.empty()) continue;
+      const BatchResult br = run_batch(job);
+      const IntegrandResult& r = br.per_integrand[0];
+      const std::size_t n_ok = trials - dead.size();
+      const std::string first = "trial " + std::to_string(dead[0]) + ": ";
+      if (n_ok >= 2) {
+        CHECK(r.ok);
+        CHECK(r.summary.per_trial.size() == n_ok);
+        CHECK(r.error.rfind("partial: " + first, 0) == 0);
+      } else {
+        CHECK(!r.ok);
+        CHECK(r.error.rfind(first, 0) == 0);
+      }
+    }
+  }
+}
+
 #define RUN(f)                                         \
   do {                                                 \
     if (std::getenv("MCB_TEST_TRACE")) {               \
@@ -458,6 +498,7 @@ int main() {
   RUN(estimator_cases);
   RUN(sampling_and_generator);
   RUN(fig1_band);
+  RUN(partial_trials);
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -174,6 +174,37 @@ def test_interpreter_values_match_reference(gpu, progs):
 
 
 @pytest.mark.gpu
+def test_eval_points_match_reference(gpu, progs):
+    """Program.evaluate (mcb_program_eval_points, the interpreter at given
+    points: the mcbatch::CompiledProgram::evaluate path) on the reference's
+    own sample points reproduces its values."""
+    for c in progs:
+        params, lo, hi = _case(c)
+        p = gpu.Program(c["source"], c["dim"], list(params))
+        pts = gpu.debug_points(c["seed"], c["index"], c["trial"], c["chunk_base"], 0, 64, lo, hi)
+        got = p.evaluate(pts, params)
+        want = np.array([fx(v) for v in c["values"]])
+        assert _values_close(got, want), c["source"]
+        # and exactly what the sampling kernels evaluate at those points
+        f = p.integrand(params, low=lo, high=hi, n_samples=c["n_samples"], index=c["index"])
+        ker = gpu.debug_eval(f, c["seed"], c["trial"], c["chunk_base"], 0, 64)
+        assert np.array_equal(np.isfinite(got), np.isfinite(ker)), c["source"]
+        fin = np.isfinite(ker)
+        assert np.array_equal(got[fin].view(np.uint64), ker[fin].view(np.uint64)), c["source"]
+
+
+@pytest.mark.gpu
+def test_parameter_scan_failing_value_raises(gpu):
+    """A scanned value whose trials all fail makes the scan throw, as in the
+    reference (src/batch.cpp:320-329 success rule, :360-364 throw)."""
+    p = gpu.Program("log(x1 - a)", 1, ["a"])
+    out, summ = gpu.parameter_scan(p, {"a": 0.0}, "a", [0.0, -1.0], trials=3, seed=4, n_samples=2000)
+    assert len(summ) == 2 and all(n == 3 for _, _, n in summ)
+    with pytest.raises(RuntimeError, match=r"parameter_scan: a#1 failed: 0 of 3"):
+        gpu.parameter_scan(p, {"a": 0.0}, "a", [0.0, 2.0], trials=3, seed=4, n_samples=2000)
+
+
+@pytest.mark.gpu
 def test_interpreter_estimates_match_reference(gpu, progs):
     for c in progs:
         params, lo, hi = _case(c)
