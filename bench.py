@@ -374,7 +374,7 @@ def fused_roofline(achieved_blocks_s, clocks):
             "peak_source": "tools/micro/split_micro.cu (1.306 blocks/clk/SM) x 148 SMs x sampled SM clock"}
 
 
-NCU_SUMMARY = "profiles/r01_bench_k_direct_ncu_summary.txt"
+NCU_SUMMARY = "profiles/r02_bench_k_direct_ncu_summary.txt"
 NCU_PIPES = "profiles/r02_k_direct_pipes.txt"
 
 
