@@ -29,22 +29,25 @@ using mcb::Method;
 using mcb::method_name;
 std::optional<Method> method_from_name(std::string_view name);
 
-struct IntegrandSpec {  // batch.hpp:22-31
-  std::string name;
-  std::string source;
-  std::size_t dim = 1;
-  HyperRect domain;
-  std::map<std::string, double> params;
-  std::uint64_t n_samples = 10000;
-  Method method = Method::Direct;
-  std::optional<RefineConfig> method_config;
+// The reference's integrand (batch.hpp:22-31): a free DSL source whose
+// parameters bind in the map's sorted name order.
+struct IntegrandSpec {
+  std::string name;                       // unique within a job
+  std::string source;                     // DSL text, e.g. "a*abs(x1+x2)"
+  std::size_t dim{1};                     // coordinates x1..x_dim
+  HyperRect domain;                       // dim-dimensional box
+  std::map<std::string, double> params;   // every free parameter of `source`
+  std::uint64_t n_samples{10000};         // per trial (the tree's total budget)
+  Method method{Method::Direct};
+  std::optional<RefineConfig> method_config;  // stratified / tree settings
 };
 
-struct JobSpec {  // batch.hpp:33-38
-  std::uint64_t seed = 0;
-  std::uint32_t trials = 1;
-  std::uint32_t workers = 0;  // GPUs (0 = every visible device)
-  std::vector<IntegrandSpec> integrands;
+// batch.hpp:33-38
+struct JobSpec {
+  std::uint64_t seed{0};
+  std::uint32_t trials{1};
+  std::uint32_t workers{0};               // GPUs here (0 = every visible device)
+  std::vector<IntegrandSpec> integrands;  // integrand_index = position
 };
 
 using mcb::Violation;

@@ -26,6 +26,9 @@ namespace mcbatch {
 
 // ---- expression tree ------------------------------------------------------------
 
+ParseError::ParseError(std::size_t at, const std::string& message)
+    : std::runtime_error(message + " (at offset " + std::to_string(at) + ")"), offset(at) {}
+
 Expr Expr::num(double v) {
   Expr e;
   e.kind = ExprKind::Number;
