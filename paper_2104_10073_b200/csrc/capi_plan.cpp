@@ -365,7 +365,15 @@ Prepared prepare(const mcb_integrand& f, uint64_t seed, uint32_t chunk_base,
   }
   const bool harm = f.family == MCB_FAMILY_HARMONIC || f.family == MCB_FAMILY_HARMONIC_VEC;
 
-  bool fast = finite && std::isfinite(xmax);
+  // MCB_FAMILY_SAFE=1 (measurement knob): every family
+  // integrand runs the SAFE variant — libdevice sincos instead of the table
+  // form, plain parameters, per-sample non-finite counting — the ablation
+  // point "accurate sincos" of DESIGN.md §3.
+  static const bool force_safe = [] {
+    const char* e = std::getenv("MCB_FAMILY_SAFE");
+    return e && *e == '1';
+  }();
+  bool fast = finite && std::isfinite(xmax) && !force_safe;
   if (fast && harm) {
     const double tmax = f.family == MCB_FAMILY_HARMONIC ? std::fabs(f.k[0]) * xmax * 1.0000001
                                                         : xmax * 1.0000001;
