@@ -21,13 +21,14 @@ using mcb::HyperRect;      // sampling.hpp:14-24
 using mcb::InvalidDomain;  // sampling.hpp:26-28
 using mcb::StreamKey;      // sampling.hpp:33-44
 
-// sampling.hpp:75-78: `count` points of rect's dimension, row-major.
+// sampling.hpp:75-78: `count` points of rect's dimension, row-major.  The
+// returning form is mcb's own (its trailing `device` defaults to 0), so that
+// argument-dependent lookup on the shared HyperRect / StreamKey types finds
+// one function, not two.
+using mcb::sample_uniform;
 inline void sample_uniform(const HyperRect& rect, const StreamKey& key, std::size_t count,
                            std::vector<double>& out) {
   out = mcb::sample_uniform(rect, key, count);
-}
-inline std::vector<double> sample_uniform(const HyperRect& rect, const StreamKey& key, std::size_t count) {
-  return mcb::sample_uniform(rect, key, count);
 }
 
 }  // namespace mcbatch

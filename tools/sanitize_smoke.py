@@ -20,8 +20,17 @@ fns = [
     mcb.stratify(prog.integrand({"a": 30.0}, n_samples=80_000, index=5)),
     mcb.tree(prog.integrand({"a": 100.0}, n_samples=60_000, index=6), samples_per_cell=512),
     mcb.stratify(mcb.harmonic(1.0, 2, n_samples=300_000, index=7), cells_per_dim=2),  # big cells: CTA tiles
+    mcb.harmonic(40.0, 4, unit_coeffs=True, n_samples=200_001, index=8),  # odd count: the tail sample
+    mcb.stratify(mcb.harmonic(9.0, 4, unit_coeffs=True, n_samples=1_000_000, index=9)),  # 8^4 cells: lane per cell
 ]
+prog4 = mcb.Program("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, ["k"])
+fns.append(mcb.stratify(prog4.integrand({"k": 9.0}, n_samples=1_000_000, index=10)))  # program lane kernel
 out = mcb.run_direct(fns, 11, 3)
 assert (out["status"] == mcb.TRIAL_OK).all(), out["status"]
+two = mcb.run_direct(fns, 11, 3, devices=[0, 0])  # (integrand, trial) sharding
+assert two.tobytes() == out.tobytes()
 st, leaves = mcb.tree_refine(fns[6], 11, 0, 0, leaves=True)
+pts = mcb.debug_points(11, 4, 0, 0, 0, 1001, [0.0, 0.0], [1.0, 1.0])
+vals = prog.evaluate(pts, {"a": 30.0})  # k_program_points, odd point count
+assert vals.shape == (1001,)
 print("ok", len(leaves), float(out["value"][0, 0]))
