@@ -21,6 +21,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 
@@ -33,17 +34,138 @@ namespace detail {
 
 constexpr int T = kProgThreads;
 
-// Operand fetch for the two samples (h = 0, 1): slots and variables live in
-// shared memory [index][h][tid]; constants and parameters are uniform.
+// Operand fetch for the NH samples of one dispatch (h = 0..NH-1): slots and
+// variables live in shared memory [index][h][tid]; constants and parameters
+// are uniform.
+template <int NH>
 __device__ __forceinline__ void fetch(uint32_t kind, uint32_t idx, const double* S, const double* X,
-                                      const double* consts, const double* params, double& v0,
-                                      double& v1) {
+                                      const double* consts, const double* params, double (&v)[NH]) {
   if (kind <= prog::kVar) {
-    const double* p = (kind == prog::kSlot ? S : X) + idx * 2 * T + threadIdx.x;
-    v0 = p[0];
-    v1 = p[T];
+    const double* p = (kind == prog::kSlot ? S : X) + idx * NH * T + threadIdx.x;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) v[h] = p[h * T];
   } else {
-    v0 = v1 = (kind == prog::kConst ? consts[idx] : params[idx]);
+    const double c = kind == prog::kConst ? consts[idx] : params[idx];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) v[h] = c;
+  }
+}
+
+template <int NH>
+__device__ __forceinline__ double fetch1(uint32_t kind, uint32_t idx, int h, const double* S, const double* X,
+                                         const double* consts, const double* params) {
+  if (kind <= prog::kVar) return (kind == prog::kSlot ? S : X)[(idx * NH + h) * T + threadIdx.x];
+  return kind == prog::kConst ? consts[idx] : params[idx];
+}
+
+// One libm-class operation on one sample.
+__device__ __forceinline__ double call_op(uint32_t op, double a, double b) {
+  switch (op) {
+    case prog::kDiv: return __ddiv_rn(a, b);
+    case prog::kPow: return pow(a, b);
+    case prog::kSin: return sin(a);
+    case prog::kCos: return cos(a);
+    case prog::kTan: return tan(a);
+    case prog::kAsin: return asin(a);
+    case prog::kAcos: return acos(a);
+    case prog::kAtan: return atan(a);
+    case prog::kExp: return exp(a);
+    case prog::kLog: return log(a);
+    case prog::kCosPlusSin: return dev::cos_plus_sin(a);
+    default: return __longlong_as_double(0x7FF8000000000000ll);
+  }
+}
+
+// The interpreter: every instruction is dispatched once for NH samples (the
+// two samples of each of NH/2 pairs), so the fetch / decode / warp-uniform
+// branch of an instruction is shared by NH evaluations.  Element-wise
+// operations run on NH register operands (NH independent FP64 chains in
+// flight); libm-class calls take the samples one at a time straight from and
+// to shared memory (code size, and no dynamically indexed register arrays).
+// Operations and their order per sample are the same for any NH.
+template <int NH>
+__device__ __forceinline__ void interp(const uint32_t* __restrict__ code, uint32_t len,
+                                       const double* __restrict__ consts, const double* __restrict__ params,
+                                       double* S, const double* X) {
+  const int tid = threadIdx.x;
+  for (uint32_t pc = 0; pc < len; ++pc) {
+    const uint32_t w0 = code[2 * pc], w1 = code[2 * pc + 1];
+    const uint32_t op = w0 & 0xFFu;
+    const uint32_t ka = (w0 >> 18) & 3u, ia = w1 & 0xFFFFu, kb = (w0 >> 20) & 3u, ib = w1 >> 16;
+    double* d = S + ((w0 >> 8) & 31u) * NH * T + tid;
+    double a[NH], b[NH], r[NH];
+    // one warp-uniform switch per instruction (a jump table), the NH samples'
+    // work inside each case
+#define MCB_UNARY(EXPR)                                       \
+  fetch<NH>(ka, ia, S, X, consts, params, a);                 \
+  _Pragma("unroll") for (int h = 0; h < NH; ++h) r[h] = (EXPR); \
+  break
+#define MCB_BINARY(EXPR)                                      \
+  fetch<NH>(ka, ia, S, X, consts, params, a);                 \
+  fetch<NH>(kb, ib, S, X, consts, params, b);                 \
+  _Pragma("unroll") for (int h = 0; h < NH; ++h) r[h] = (EXPR); \
+  break
+    switch (op) {
+      case prog::kCopy: MCB_UNARY(a[h]);
+      case prog::kNeg: MCB_UNARY(-a[h]);
+      case prog::kAdd: MCB_BINARY(__dadd_rn(a[h], b[h]));
+      case prog::kSub: MCB_BINARY(__dsub_rn(a[h], b[h]));
+      case prog::kMul: MCB_BINARY(__dmul_rn(a[h], b[h]));
+      case prog::kSqrt: MCB_UNARY(__dsqrt_rn(a[h]));
+      case prog::kAbs: MCB_UNARY(fabs(a[h]));
+      case prog::kFloor: MCB_UNARY(floor(a[h]));
+      case prog::kMin: MCB_BINARY(fmin(a[h], b[h]));
+      case prog::kMax: MCB_BINARY(fmax(a[h], b[h]));
+      case prog::kCosPlusSin: {  // the table form for NH samples at once, libm for the rare rest
+        fetch<NH>(ka, ia, S, X, consts, params, a);
+        uint32_t in_range = 0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const bool in = dev::cos_plus_sin_in_range(a[h]);
+          r[h] = dev::cos_plus_sin_table(in ? a[h] : 0.0);
+          in_range |= in ? 1u << h : 0u;
+        }
+        if (in_range != (1u << NH) - 1u) {  // operands still intact: nothing stored yet
+#pragma unroll 1
+          for (int h = 0; h < NH; ++h)
+            if (!(in_range >> h & 1u)) d[h * T] = dev::cos_plus_sin_libm(fetch1<NH>(ka, ia, h, S, X, consts, params));
+        }
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          if (in_range >> h & 1u) d[h * T] = r[h];
+        continue;
+      }
+      case prog::kSinCos: {
+        double* d2 = S + ((w0 >> 13) & 31u) * NH * T + tid;
+#pragma unroll 1
+        for (int h = 0; h < NH; ++h) {
+          double sn, cs;
+          sincos(fetch1<NH>(ka, ia, h, S, X, consts, params), &sn, &cs);
+          d[h * T] = sn;
+          d2[h * T] = cs;
+        }
+        continue;
+      }
+      case prog::kDiv: case prog::kPow: case prog::kSin: case prog::kCos: case prog::kTan:
+      case prog::kAsin: case prog::kAcos: case prog::kAtan: case prog::kExp: case prog::kLog: {
+        const bool binary = op == prog::kDiv || op == prog::kPow;
+#pragma unroll 1
+        for (int h = 0; h < NH; ++h) {
+          const double x = fetch1<NH>(ka, ia, h, S, X, consts, params);
+          const double y = binary ? fetch1<NH>(kb, ib, h, S, X, consts, params) : 0.0;
+          d[h * T] = call_op(op, x, y);
+        }
+        continue;
+      }
+      default:
+#pragma unroll
+        for (int h = 0; h < NH; ++h) r[h] = __longlong_as_double(0x7FF8000000000000ll);
+        break;
+    }
+#undef MCB_UNARY
+#undef MCB_BINARY
+#pragma unroll
+    for (int h = 0; h < NH; ++h) d[h * T] = r[h];
   }
 }
 
@@ -51,81 +173,38 @@ __device__ __forceinline__ void interp_pair(const uint32_t* __restrict__ code, u
                                             const double* __restrict__ consts,
                                             const double* __restrict__ params, double* S,
                                             const double* X) {
-  const int tid = threadIdx.x;
-  for (uint32_t pc = 0; pc < len; ++pc) {
-    const uint32_t w0 = code[2 * pc], w1 = code[2 * pc + 1];
-    const uint32_t op = w0 & 0xFFu;
-    double a0, a1, b0 = 0.0, b1 = 0.0, r0, r1;
-    fetch((w0 >> 18) & 3u, w1 & 0xFFFFu, S, X, consts, params, a0, a1);
-    switch (op) {
-      case prog::kAdd: case prog::kSub: case prog::kMul: case prog::kDiv:
-      case prog::kPow: case prog::kMin: case prog::kMax:
-        fetch((w0 >> 20) & 3u, w1 >> 16, S, X, consts, params, b0, b1);
-        break;
-      default:
-        break;
-    }
-    switch (op) {
-      case prog::kCopy: r0 = a0; r1 = a1; break;
-      case prog::kSinCos: {
-        double c0, c1;
-        sincos(a0, &r0, &c0);
-        sincos(a1, &r1, &c1);
-        double* d2 = S + ((w0 >> 13) & 31u) * 2 * T + tid;
-        d2[0] = c0;
-        d2[T] = c1;
-      } break;
-      case prog::kNeg: r0 = -a0; r1 = -a1; break;
-      case prog::kAdd: r0 = __dadd_rn(a0, b0); r1 = __dadd_rn(a1, b1); break;
-      case prog::kSub: r0 = __dsub_rn(a0, b0); r1 = __dsub_rn(a1, b1); break;
-      case prog::kMul: r0 = __dmul_rn(a0, b0); r1 = __dmul_rn(a1, b1); break;
-      case prog::kDiv: r0 = __ddiv_rn(a0, b0); r1 = __ddiv_rn(a1, b1); break;
-      case prog::kPow: r0 = pow(a0, b0); r1 = pow(a1, b1); break;
-      case prog::kSin: r0 = sin(a0); r1 = sin(a1); break;
-      case prog::kCos: r0 = cos(a0); r1 = cos(a1); break;
-      case prog::kTan: r0 = tan(a0); r1 = tan(a1); break;
-      case prog::kAsin: r0 = asin(a0); r1 = asin(a1); break;
-      case prog::kAcos: r0 = acos(a0); r1 = acos(a1); break;
-      case prog::kAtan: r0 = atan(a0); r1 = atan(a1); break;
-      case prog::kExp: r0 = exp(a0); r1 = exp(a1); break;
-      case prog::kLog: r0 = log(a0); r1 = log(a1); break;
-      case prog::kSqrt: r0 = __dsqrt_rn(a0); r1 = __dsqrt_rn(a1); break;
-      case prog::kAbs: r0 = fabs(a0); r1 = fabs(a1); break;
-      case prog::kFloor: r0 = floor(a0); r1 = floor(a1); break;
-      case prog::kMin: r0 = fmin(a0, b0); r1 = fmin(a1, b1); break;
-      case prog::kMax: r0 = fmax(a0, b0); r1 = fmax(a1, b1); break;
-      case prog::kCosPlusSin: r0 = dev::cos_plus_sin(a0); r1 = dev::cos_plus_sin(a1); break;
-      default: r0 = r1 = __longlong_as_double(0x7FF8000000000000ll); break;
-    }
-    double* d = S + ((w0 >> 8) & 31u) * 2 * T + tid;
-    d[0] = r0;
-    d[T] = r1;
-  }
+  interp<2>(code, len, consts, params, S, X);
 }
 
-// Coordinates of the two samples of pair q into X[j][h][tid].
-template <int D, bool UNIT_DOM>
-__device__ __forceinline__ void gen_points(const FnDesc& f, const PhiloxPrefix& P, uint32_t q,
-                                           double* X) {
-  const uint64_t pbase = uint64_t(dev::kM0) * uint64_t(q * uint32_t(D));
+// Coordinates of the two samples of each of the NP pairs q0 + i*stride
+// (i < NP) into X[j][2i + h][tid] (NH = 2 NP samples per dispatch).
+template <int D, bool UNIT_DOM, int NP = 1>
+__device__ __forceinline__ void gen_points(const FnDesc& f, const PhiloxPrefix& P, uint32_t q0,
+                                           double* X, uint32_t stride = 0) {
+  constexpr int NH = 2 * NP;
 #pragma unroll
-  for (int i = 0; i < D; ++i) {
-    uint32_t o[4];
-    dev::philox_block_p(P, pbase + uint64_t(i) * dev::kM0, o);
+  for (int pi = 0; pi < NP; ++pi) {
+    const uint64_t pbase = uint64_t(dev::kM0) * uint64_t((q0 + uint32_t(pi) * stride) * uint32_t(D));
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int t = 2 * i + hh, h = t / D, j = t % D;
-      const double u = __dmul_rn(hh ? dev::u_scaled(o[2], o[3]) : dev::u_scaled(o[0], o[1]),
-                                 dev::kTwoM64);
-      const double x = UNIT_DOM ? u : __dadd_rn(f.low[j], __dmul_rn(f.width[j], u));
-      X[(j * 2 + h) * T + threadIdx.x] = x;
+    for (int i = 0; i < D; ++i) {
+      uint32_t o[4];
+      dev::philox_block_p(P, pbase + uint64_t(i) * dev::kM0, o);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int t = 2 * i + hh, h = t / D, j = t % D;
+        const double u = __dmul_rn(hh ? dev::u_scaled(o[2], o[3]) : dev::u_scaled(o[0], o[1]),
+                                   dev::kTwoM64);
+        const double x = UNIT_DOM ? u : __dadd_rn(f.low[j], __dmul_rn(f.width[j], u));
+        X[(j * NH + 2 * pi + h) * T + threadIdx.x] = x;
+      }
     }
   }
 }
 
-// Shared memory: S[slots][2][T] | X[D][2][T] | consts[kMaxConsts] | code[2 * kMaxCode]
-__host__ __device__ constexpr size_t program_smem_bytes(uint32_t slots, int dim) {
-  return (size_t(slots) + size_t(dim)) * 2 * T * sizeof(double) + prog::kMaxConsts * sizeof(double) +
+// Shared memory: S[slots][NH][T] | X[D][NH][T] | consts[kMaxConsts] | code[2 * kMaxCode]
+// (NH = 2 NP samples per dispatch)
+__host__ __device__ constexpr size_t program_smem_bytes(uint32_t slots, int dim, int np = 1) {
+  return (size_t(slots) + size_t(dim)) * 2 * size_t(np) * T * sizeof(double) + prog::kMaxConsts * sizeof(double) +
          2 * prog::kMaxCode * sizeof(uint32_t);
 }
 
@@ -136,15 +215,15 @@ struct ProgramSmem {
   uint32_t* code;
 };
 
-template <int D>
+template <int D, int NP = 1>
 __device__ __forceinline__ ProgramSmem stage_program(const FnDesc& f, const uint32_t* __restrict__ code,
                                                      const double* __restrict__ consts, uint32_t slots,
                                                      double* params) {
   extern __shared__ double dyn[];
   ProgramSmem m;
   m.S = dyn;
-  m.X = dyn + size_t(slots) * 2 * T;
-  m.consts = m.X + size_t(D) * 2 * T;
+  m.X = dyn + size_t(slots) * 2 * NP * T;
+  m.consts = m.X + size_t(D) * 2 * NP * T;
   m.code = reinterpret_cast<uint32_t*>(m.consts + prog::kMaxConsts);
   for (uint32_t i = threadIdx.x; i < 2 * f.prog_len; i += T) m.code[i] = code[f.prog_off + i];
   for (uint32_t i = threadIdx.x; i < f.n_consts; i += T) m.consts[i] = consts[f.const_off + i];
@@ -157,7 +236,10 @@ __device__ __forceinline__ ProgramSmem stage_program(const FnDesc& f, const uint
   return m;
 }
 
-template <int D, int V>
+// NP pairs per thread per dispatch (NH = 2 NP samples): thread tid takes the
+// pairs q = tid + i T in ascending i exactly as with NP = 1, so its sums (and
+// the results) do not depend on NP.
+template <int D, int V, int NP>
 __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
                                                const uint32_t* __restrict__ tile_fn, uint64_t tile0,
                                                TilePartial* __restrict__ part,
@@ -184,12 +266,13 @@ __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
   const PhiloxPrefix P =
       dev::make_prefix(f.key0, f.key1, f.chunk_base + chunk, f.trial_base + trial);
   __shared__ double params[prog::kMaxParams];
-  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  const ProgramSmem m = stage_program<D, NP>(f, code, consts, slots, params);
+  constexpr int NH = 2 * NP;
   if (STRAT) {  // per-tile shift = f(first sample of the tile)
     __shared__ double s_shift;
     if (threadIdx.x == 0) {
-      gen_points<D, false>(f, P, 0, m.X);
-      interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
+      gen_points<D, false, NP>(f, P, 0, m.X, T);
+      interp<NH>(m.code, f.prog_len, m.consts, params, m.S, m.X);
       const double f0 = m.S[0];
       s_shift = finite64(f0) ? f0 : 0.0;
     }
@@ -199,19 +282,24 @@ __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
 
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
-  for (uint32_t q = threadIdx.x; q < pairs; q += T) {
-    gen_points<D, UNIT_DOM>(f, P, q, m.X);
-    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
-    const double f0 = m.S[threadIdx.x], f1 = m.S[T + threadIdx.x];
-    const bool has1 = 2 * q + 1 < count;
-    const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
-    nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
-    const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
-    const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
-    s1 = __dadd_rn(s1, g0);
-    s2 = fma(g0, g0, s2);
-    s1 = __dadd_rn(s1, g1);
-    s2 = fma(g1, g1, s2);
+  for (uint32_t q0 = threadIdx.x; q0 < pairs; q0 += NP * T) {
+    gen_points<D, UNIT_DOM, NP>(f, P, q0, m.X, T);
+    interp<NH>(m.code, f.prog_len, m.consts, params, m.S, m.X);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const uint32_t q = q0 + uint32_t(i) * T;
+      if (q >= pairs) break;
+      const double f0 = m.S[2 * i * T + threadIdx.x], f1 = m.S[(2 * i + 1) * T + threadIdx.x];
+      const bool has1 = 2 * q + 1 < count;
+      const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
+      nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+      const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
+      const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
+      s1 = __dadd_rn(s1, g0);
+      s2 = fma(g0, g0, s2);
+      s1 = __dadd_rn(s1, g1);
+      s2 = fma(g1, g1, s2);
+    }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -426,20 +514,36 @@ using ProgFn = void (*)(const FnDesc*, const uint32_t*, uint64_t, TilePartial*, 
 using ProgEvalFn = void (*)(const FnDesc*, const uint32_t*, const double*, uint32_t, uint32_t,
                             uint32_t, uint32_t, uint32_t, double*);
 
+// Pairs per dispatch of the CTA-per-tile kernels (modes 0-2): index of
+// NP = 1, 2, 4.
+constexpr int kNpVariants = 3;
+constexpr int np_of(int i) { return 1 << i; }
+
 struct ProgEntry {
-  ProgFn run = nullptr;
+  ProgFn run = nullptr;               // NP = 1 (every mode)
+  ProgFn run_np[kNpVariants] = {};    // modes 0-2 by NP index
   ProgEvalFn eval = nullptr;
 };
 
 struct ProgTable {
   ProgEntry e[MCB_MAX_DIM + 1][5];  // by program_kernel_mode: general / unit domain, cells, small cells (warp, lane)
+  template <int D, int V>
+  static ProgEntry tile_entry(ProgEvalFn eval) {
+    ProgEntry p;
+    p.run = k_program<D, V, 1>;
+    p.run_np[0] = k_program<D, V, 1>;
+    p.run_np[1] = k_program<D, V, 2>;
+    p.run_np[2] = k_program<D, V, 4>;
+    p.eval = eval;
+    return p;
+  }
   template <int D>
   void put() {
-    e[D][0] = {k_program<D, kSafe>, k_program_eval<D, kSafe>};
-    e[D][1] = {k_program<D, kSafe | kUnitDomain>, k_program_eval<D, kSafe | kUnitDomain>};
-    e[D][2] = {k_program<D, kSafe | kStrat>, k_program_eval<D, kSafe>};
-    e[D][3] = {k_program_warp<D, kSafe | kStrat | kWarpTile>, k_program_eval<D, kSafe>};
-    e[D][4] = {k_program_lane<D, kSafe | kStrat | kLaneCell>, k_program_eval<D, kSafe>};
+    e[D][0] = tile_entry<D, kSafe>(k_program_eval<D, kSafe>);
+    e[D][1] = tile_entry<D, kSafe | kUnitDomain>(k_program_eval<D, kSafe | kUnitDomain>);
+    e[D][2] = tile_entry<D, kSafe | kStrat>(k_program_eval<D, kSafe>);
+    e[D][3] = {k_program_warp<D, kSafe | kStrat | kWarpTile>, {}, k_program_eval<D, kSafe>};
+    e[D][4] = {k_program_lane<D, kSafe | kStrat | kLaneCell>, {}, k_program_eval<D, kSafe>};
   }
   ProgTable() {
     put<1>();
@@ -475,12 +579,37 @@ static cudaError_t ensure_smem_optin() {
       if ((e = cudaFuncSetAttribute(t.e[d][v].run, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem)) != cudaSuccess)
         return e;
+      for (int i = 0; i < kNpVariants; ++i)
+        if (t.e[d][v].run_np[i] &&
+            (e = cudaFuncSetAttribute(t.e[d][v].run_np[i], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(program_smem_bytes(prog::kMaxDepth, d, np_of(i))))) != cudaSuccess)
+          return e;
       if ((e = cudaFuncSetAttribute(t.e[d][v].eval, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem)) != cudaSuccess)
         return e;
     }
   done.insert(dev);
   return cudaSuccess;
+}
+
+// Pairs per dispatch for a group (CTA-per-tile modes 0-2): the largest NP
+// whose stack + coordinates fit kInterpSmemBudget, so a few CTAs stay
+// resident per SM; MCB_INTERP_NP=1|2|4 forces it (ablation).
+constexpr size_t kInterpSmemBudget = 56 * 1024;
+static int interp_np_index(uint32_t slots, int dim, int mode) {
+  if (mode > 2) return 0;
+  static const int forced = [] {
+    const char* v = std::getenv("MCB_INTERP_NP");
+    return v ? std::atoi(v) : 0;
+  }();
+  for (int i = kNpVariants - 1; i > 0; --i) {
+    if (forced) {
+      if (np_of(i) == forced) return i;
+      continue;
+    }
+    if (program_smem_bytes(slots, dim, np_of(i)) <= kInterpSmemBudget) return i;
+  }
+  return 0;
 }
 
 static const ProgEntry* prog_entry(int dim, int variant) {
@@ -504,11 +633,13 @@ cudaError_t launch_program_group(const GroupLaunch& g, const FnDesc* fns, const 
       return err;
   }
   if (cudaError_t err = ensure_smem_optin(); err != cudaSuccess) return err;
-  const size_t smem = program_smem_bytes(g.slots, g.dim);
+  const int npi = interp_np_index(g.slots, g.dim, program_kernel_mode(g.variant));
+  const ProgFn run = e->run_np[npi] ? e->run_np[npi] : e->run;
+  const size_t smem = program_smem_bytes(g.slots, g.dim, e->run_np[npi] ? np_of(npi) : 1);
   for (uint64_t off = 0; off < n_ctas; off += kMaxGrid) {
     const uint64_t n = n_ctas - off < kMaxGrid ? n_ctas - off : kMaxGrid;
-    e->run<<<dim3(uint32_t(n)), dim3(T), smem, s>>>(fns, tile_fn, g.tile0 + off * per_cta, part, code,
-                                                      consts, g.slots);
+    run<<<dim3(uint32_t(n)), dim3(T), smem, s>>>(fns, tile_fn, g.tile0 + off * per_cta, part, code,
+                                                   consts, g.slots);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }

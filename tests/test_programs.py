@@ -449,3 +449,47 @@ def test_parameter_scan_matches_reference(gpu):
     assert np.all(np.abs(out["value"] - ref["value"]) <= 1e-12 + 1e-9 * np.abs(ref["value"]))
     assert np.allclose([s[0] for s in summaries], mean, rtol=1e-9, atol=1e-12)
     assert all(s[2] == 3 for s in summaries)
+
+
+_NP_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, sys.argv[1])
+import paper_2104_10073_b200 as mcb
+mcb.program_jit(0)
+srcs = [("cos(k*(x1+x2+x3+x4)) + sin(k*(x1+x2+x3+x4))", 4, {"k": 31.5}),
+        ("exp(-3*(x1-0.4)^2) * cos(5*x2) + x3 / (x1 - 0.5)", 3, {}),
+        ("pow(x1, a) * log(x2) + sqrt(x1*x2) - floor(3*x3) + min(x1, x2) * max(x2, x3) + tan(x1)", 3, {"a": 1.5}),
+        ("cos(1e7*x1) + sin(1e7*x1) + sin(x2)*cos(x2) + asin(x1) + acos(x2) + atan(x1/x2)", 2, {}),
+        ("((x1+x2)*(x3+x4))/((x5-x6)*(x7+x8)) + ((x1*x2)+(x3*x4))*((x5*x6)-(x7*x8))", 8, {})]
+keep, fns = [], []
+for i, (s, d, p) in enumerate(srcs):
+    prog = mcb.Program(s, d, sorted(p))
+    keep.append(prog)
+    fns.append(prog.integrand(p, n_samples=150_001, index=i))
+    fns.append(prog.integrand(p, low=[-0.5] * d, high=[1.5] * d, n_samples=70_000, index=10 + i))
+fns.append(mcb.stratify(keep[1].integrand({}, low=[-1, 0, 0], high=[1, 2, 1], n_samples=300_000, index=30),
+                        cells_per_dim=2))
+out = mcb.run_direct(fns, 4242, 3)
+print(hashlib.sha256(out.tobytes()).hexdigest())
+"""
+
+
+@pytest.mark.gpu
+def test_interpreter_pairs_per_dispatch_bit_identical(tmp_path):
+    """The bytecode interpreter dispatches each instruction for NP pairs at
+    once (1, 2 or 4 by the program's shared-memory need); a thread still takes
+    its pairs in ascending order, so every McEstimate is byte-identical for
+    any NP (forced per process with MCB_INTERP_NP; JIT off)."""
+    import subprocess
+    import sys
+    script = tmp_path / "np.py"
+    script.write_text(_NP_SCRIPT)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = []
+    for np_ in ("1", "2", "4"):
+        env = dict(os.environ, MCB_INTERP_NP=np_, MCB_PROGRAM_JIT="0")
+        r = subprocess.run([sys.executable, str(script), root], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        digests.append(r.stdout.split()[-1])
+    assert digests[0] == digests[1] == digests[2], digests
