@@ -296,9 +296,14 @@ struct Lowering {
     return int(nodes.size() - 1);
   }
 
-  bool is_const(int node, double v) const {
+  const double* const_of(int node) const {
     const DagNode& n = nodes[size_t(node)];
-    return n.leaf && n.leaf_op.kind == kConst && p.consts[n.leaf_op.index] == v;
+    return n.leaf && n.leaf_op.kind == kConst ? &p.consts[n.leaf_op.index] : nullptr;
+  }
+
+  bool is_const(int node, double v) const {
+    const double* c = const_of(node);
+    return c && *c == v;
   }
 
   int leaf(uint32_t kind, uint32_t idx) {
@@ -327,6 +332,7 @@ struct Lowering {
         DagNode d;
         d.op = kNeg;
         d.a = lower(*n.kids[0]);
+        if (const double* v = const_of(d.a)) return leaf(kConst, constant(-*v));  // exact
         return intern(d);
       }
       case Node::Bin:
@@ -343,6 +349,14 @@ struct Lowering {
         if (d.op == kPow && is_const(d.b, 2.0)) {
           d.op = kMul;
           d.b = d.a;
+        }
+        // constant operands of + - * /: one correctly rounded IEEE operation,
+        // the same on the host as on the device (2*pi*x1 = (2*pi)*x1)
+        const double *ca = const_of(d.a), *cb = d.b >= 0 ? const_of(d.b) : nullptr;
+        if (ca && cb && (d.op == kAdd || d.op == kSub || d.op == kMul || d.op == kDiv)) {
+          const double x = *ca, y = *cb;
+          const double r = d.op == kAdd ? x + y : d.op == kSub ? x - y : d.op == kMul ? x * y : x / y;
+          return leaf(kConst, constant(r));
         }
         return intern(d);
       }

@@ -89,6 +89,13 @@ def test_compiler_contract(mcb):
     assert len(dsl.Program(p.source, 4, {"k": 1.0}).code) == 21
     assert (p.n_instr, p.depth) == (5, 1)
     assert mcb.Program("a*x1 + b + c", 1, ["c", "a", "b"]).param_names == ["a", "b", "c"]
+    # squares compile to one multiply of the shared operand (x1-c computed once):
+    # Sub, Mul, Sub, Mul, Add, Mul(-100), Exp; other exponents stay pow
+    peak = mcb.Program("exp(-100*((x1-c)^2+(x2-c)^2))", 2, ["c"])
+    assert (peak.n_instr, peak.depth) == (7, 2)
+    assert mcb.Program("pow(x1-c, 2)", 1, ["c"]).n_instr == 2
+    assert mcb.Program("(x1-c)^3", 1, ["c"]).n_instr == 2
+    assert mcb.Program("(x1-c)^2.5", 1, ["c"]).n_instr == 2
     cases = {
         "x3": "x3 exceeds dim=2",
         "2+": "expression does not parse: expected a number, identifier or '(' (at offset 2)",
@@ -191,6 +198,30 @@ def test_eval_points_match_reference(gpu, progs):
         assert np.array_equal(np.isfinite(got), np.isfinite(ker)), c["source"]
         fin = np.isfinite(ker)
         assert np.array_equal(got[fin].view(np.uint64), ker[fin].view(np.uint64)), c["source"]
+
+
+@pytest.mark.gpu
+def test_squares_and_constant_folding_exact(gpu):
+    """E^2 / pow(E, 2) run as E*E and constant sub-expressions are folded on
+    the host: both are single correctly rounded IEEE operations, so the GPU
+    values equal numpy's bit for bit, specials included."""
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.uniform(-3, 3, 200), [0.0, -0.0, 1e200, -1e200, 1e-170, np.inf, -np.inf, np.nan]])
+    pts = x.reshape(-1, 1)
+    c = 0.3125
+    cases = [("(x1-c)^2", lambda v: (v - c) * (v - c)),
+             ("pow(x1-c, 2)", lambda v: (v - c) * (v - c)),
+             ("2*pi*x1", lambda v: (2 * math.pi) * v),
+             ("-100*x1 + 1/3", lambda v: -100.0 * v + 1.0 / 3.0),
+             ("x1*2*pi", lambda v: (v * 2) * math.pi)]
+    for src, ref in cases:
+        p = gpu.Program(src, 1, ["c"] if "c" in src.replace("pi", "") else [])
+        got = p.evaluate(pts, {"c": c} if p.param_names else None)
+        with np.errstate(all="ignore"):
+            want = ref(x)
+        assert np.array_equal(np.isnan(got), np.isnan(want)), src
+        ok = ~np.isnan(want)
+        assert np.array_equal(got[ok].view(np.uint64), want[ok].view(np.uint64)), src
 
 
 @pytest.mark.gpu
