@@ -245,6 +245,26 @@ MCB_API mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64
 MCB_API mcb_status mcb_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
                          uint64_t chunk_base, int device, mcb_trial_stats* out);
 
+/* One chunk's accumulator = reference ChunkAccum (include/mcbatch/estimator.hpp:
+ * 60-68): finite-sample count, non-finite count, mean and sum of squared
+ * deviations of the chunk's f values. */
+typedef struct mcb_chunk_accum {
+  uint64_t n;
+  uint64_t n_nonfinite;
+  double mean;
+  double m2;
+} mcb_chunk_accum;
+
+/* accumulate_chunk (include/mcbatch/estimator.hpp:70-74, src/estimator.cpp:
+ * 36-49): the first `count` (<= 65536) points of the stream {seed,
+ * fn->integrand_index, trial, chunk} on fn's domain, evaluated and reduced on
+ * `device` (one tile of the fused kernel).  n and n_nonfinite are exact;
+ * mean and m2 come from the tile's shifted sums (mean = c + S1/n, m2 = S2 -
+ * S1*S1/n), within ~1e-15 relative of the reference's Welford recurrence. */
+MCB_API mcb_status mcb_accumulate_chunk(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
+                                        uint64_t chunk, uint32_t count, int device,
+                                        mcb_chunk_accum* out);
+
 /* tree_refine (src/estimator.cpp:212-318) for one integrand (method TREE,
  * n_samples = total_budget) and key base {seed, fn->integrand_index, trial,
  * chunk_base}.  Cells are estimated on `device`.  `leaves` (may be NULL)

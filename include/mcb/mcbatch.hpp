@@ -199,6 +199,27 @@ std::vector<TrialSummary> parameter_scan(const IntegrandSpec& tmpl, const std::s
 McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const StreamKey& key_base,
                      int device = 0);
 
+// include/mcbatch/estimator.hpp:59-68: one chunk's accumulator.  add / merge
+// are the reference's host recurrences (src/estimator.cpp:9-34).
+struct ChunkAccum {
+  std::uint64_t n = 0;
+  std::uint64_t n_nonfinite = 0;
+  double mean = 0.0;
+  double m2 = 0.0;
+
+  void add(double x);
+  void merge(const ChunkAccum& other);
+};
+
+// src/estimator.cpp:36-49: the chunk `key` (count <= kChunkSize points of the
+// spec's domain) as one tile of the fused kernel on `device` (mcb_accumulate_chunk).
+ChunkAccum accumulate_chunk(const IntegrandSpec& spec, const StreamKey& key, std::size_t count,
+                            int device = 0);
+
+// src/estimator.cpp:55-73: chunks merged in the given order, then the
+// McEstimate; throws AllSamplesNonFinite when no finite sample survived.
+McEstimate reduce_chunks(double volume, std::span<const ChunkAccum> chunks);
+
 // include/mcbatch/estimator.hpp:33-38
 struct StratumNode {
   HyperRect cell;

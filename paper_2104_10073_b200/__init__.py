@@ -77,6 +77,12 @@ class TrialStats(ctypes.Structure):
                 ("budget_exhausted", ctypes.c_uint32), ("max_depth", ctypes.c_uint32)]
 
 
+class ChunkAccum(ctypes.Structure):
+    """``mcb_chunk_accum`` = reference ChunkAccum (include/mcbatch/estimator.hpp:60-68)."""
+    _fields_ = [("n", ctypes.c_uint64), ("n_nonfinite", ctypes.c_uint64),
+                ("mean", ctypes.c_double), ("m2", ctypes.c_double)]
+
+
 class Leaf(ctypes.Structure):
     """``mcb_leaf`` = reference StratumNode (include/mcbatch/estimator.hpp:33-38)."""
     _fields_ = [("low", ctypes.c_double * MAX_DIM), ("high", ctypes.c_double * MAX_DIM),
@@ -109,7 +115,7 @@ ABI_SYMBOLS = [
     "mcb_probe_philox_peak", "mcb_program_compile", "mcb_program_destroy", "mcb_program_info",
     "mcb_program_param_name", "mcb_stratified_plan", "mcb_tree_refine", "mcb_program_jit",
     "mcb_program_jit_compiles", "mcb_program_jit_error", "mcb_program_jit_build", "mcb_stratified_mc",
-    "mcb_program_eval_points",
+    "mcb_program_eval_points", "mcb_accumulate_chunk",
 ]
 
 
@@ -134,6 +140,7 @@ def _load() -> ctypes.CDLL:
         "mcb_summarize_trials": (i32, [P(TrialStats), u32, P(dbl), P(dbl), P(u32)]),
         "mcb_run_direct": (i32, [P(Integrand), sz, u64, u32, P(i32), i32, vp, P(dbl)]),
         "mcb_direct_mc": (i32, [P(Integrand), u64, u32, u64, i32, P(TrialStats)]),
+        "mcb_accumulate_chunk": (i32, [P(Integrand), u64, u32, u64, u32, i32, P(ChunkAccum)]),
         "mcb_plan_create": (i32, [P(Integrand), sz, u64, u32, i32, P(vp)]),
         "mcb_plan_launch": (i32, [vp, vp]),
         "mcb_plan_download": (i32, [vp, vp, vp]),
@@ -406,6 +413,15 @@ def direct_mc(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, devi
     st = TrialStats()
     _check(lib.mcb_direct_mc(ctypes.byref(f), seed, trial, chunk_base, device, ctypes.byref(st)))
     return st
+
+
+def accumulate_chunk(f: Integrand, seed: int, trial: int, chunk: int, count: int,
+                     device: int = 0) -> ChunkAccum:
+    """accumulate_chunk (ref src/estimator.cpp:36-49): one chunk's (n, n_nonfinite,
+    mean, m2) of the stream {seed, f.integrand_index, trial, chunk}, on the GPU."""
+    acc = ChunkAccum()
+    _check(lib.mcb_accumulate_chunk(ctypes.byref(f), seed, trial, chunk, count, device, ctypes.byref(acc)))
+    return acc
 
 
 def tree_refine(f: Integrand, seed: int, trial: int = 0, chunk_base: int = 0, device: int = 0,

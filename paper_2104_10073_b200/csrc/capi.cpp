@@ -511,6 +511,36 @@ mcb_status mcb_direct_mc(const mcb_integrand* fn, uint64_t seed, uint32_t trial,
   return run_shard(&f, 1, seed, 1, device, out, &cb, &tb);
 }
 
+mcb_status mcb_accumulate_chunk(const mcb_integrand* fn, uint64_t seed, uint32_t trial, uint64_t chunk,
+                                uint32_t count, int device, mcb_chunk_accum* out) {
+  if (!fn || !out) return fail(MCB_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (count > MCB_CHUNK_SIZE) return fail(MCB_ERR_INVALID_ARGUMENT, "count exceeds the chunk size 65536");
+  if (chunk > 0xFFFFFFFFull) return fail(MCB_ERR_OUT_OF_RANGE, "chunk_index exceeds 32 bits");
+  mcb_integrand f = *fn;  // one chunk of the direct method
+  f.method = MCB_METHOD_DIRECT;
+  f.n_samples = count < 2 ? 2 : count;  // the job rules (n_samples >= 2) are not accumulate_chunk's
+  mcb_status st = validate_for_run(&f, 1, 1);
+  if (st != MCB_OK) return st;
+  *out = mcb_chunk_accum{0, 0, 0.0, 0.0};
+  if (count == 0) return MCB_OK;
+  if ((st = check_device(device)) != MCB_OK) return st;
+  f.n_samples = count;
+  const uint32_t cb = uint32_t(chunk), tb = trial;
+  mcb_trial_stats stats;
+  TilePartial p;
+  if ((st = run_shard(&f, 1, seed, 1, device, &stats, &cb, &tb, &p, 1)) != MCB_OK) return st;
+  // the tile's sums about its shift c -> (mean, m2), as k_combine's merge_tile
+  out->n = p.n_finite;
+  out->n_nonfinite = p.n_nonfinite;
+  if (p.n_finite) {
+    const double n = double(p.n_finite), dev = p.s1 / n;
+    const double m2 = p.s2 - p.s1 * dev;
+    out->mean = p.shift + dev;
+    out->m2 = m2 > 0.0 ? m2 : (m2 == m2 ? 0.0 : HUGE_VAL);
+  }
+  return MCB_OK;
+}
+
 mcb_status mcb_debug_points(uint64_t seed, uint32_t integrand_index, uint32_t trial, uint64_t chunk,
                             uint64_t first_point, uint64_t count, uint32_t dim, const double* low,
                             const double* high, int device, double* out) {

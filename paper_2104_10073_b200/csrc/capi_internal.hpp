@@ -190,7 +190,8 @@ mcb_status enqueue_run(const HostPlan& hp, DevBuf& buf, uint32_t trials, const F
 DeviceCtx& device_ctx(int device);
 mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials, int device,
                      mcb_trial_stats* out, const uint32_t* chunk_bases = nullptr,
-                     const uint32_t* trial_bases = nullptr);
+                     const uint32_t* trial_bases = nullptr, TilePartial* tile_out = nullptr,
+                     size_t tile_cap = 0);
 
 // ---- capi_tree.cpp: tree rounds ----------------------------------------------
 mcb_status run_cells(const std::vector<mcb::tree::CellBatch>& batches, uint64_t seed,

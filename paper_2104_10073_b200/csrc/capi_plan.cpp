@@ -652,9 +652,11 @@ DeviceCtx& device_ctx(int device) {
 
 
 // One shard of mcb_run_direct on one device (synchronous).
+// tile_out (may be NULL): also returns the first tile_cap raw tile partials
+// (the chunk accumulators of mcb_accumulate_chunk).
 mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
                      int device, mcb_trial_stats* out, const uint32_t* chunk_bases,
-                     const uint32_t* trial_bases) {
+                     const uint32_t* trial_bases, TilePartial* tile_out, size_t tile_cap) {
   HostPlan hp;
   const auto tb0 = std::chrono::steady_clock::now();
   mcb_status st = build_host_plan(fns, n_fns, seed, trials, 0, 0, hp, chunk_bases, trial_bases);
@@ -690,6 +692,10 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
   if ((e = cudaMemcpyAsync(c.h_out, c.buf.out, sizeof(mcb_trial_stats) * n_out, cudaMemcpyDeviceToHost,
                            c.stream)) != cudaSuccess)
     return cuda_fail(e, "cudaMemcpyAsync(results)");
+  if (tile_out && tile_cap &&
+      (e = cudaMemcpyAsync(tile_out, c.buf.part, sizeof(TilePartial) * std::min<size_t>(tile_cap, hp.n_tiles),
+                           cudaMemcpyDeviceToHost, c.stream)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpyAsync(tile partials)");
   if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   std::memcpy(out, c.h_out, sizeof(mcb_trial_stats) * n_out);
   return MCB_OK;

@@ -507,6 +507,47 @@ StratumNode node_of(const mcb::StratumNode& n) { return StratumNode{n.cell, n.es
 
 }  // namespace
 
+void ChunkAccum::add(double x) {
+  mcb::ChunkAccum a{n, n_nonfinite, mean, m2};
+  a.add(x);
+  *this = ChunkAccum{a.n, a.n_nonfinite, a.mean, a.m2};
+}
+
+void ChunkAccum::merge(const ChunkAccum& other) {
+  mcb::ChunkAccum a{n, n_nonfinite, mean, m2};
+  a.merge(mcb::ChunkAccum{other.n, other.n_nonfinite, other.mean, other.m2});
+  *this = ChunkAccum{a.n, a.n_nonfinite, a.mean, a.m2};
+}
+
+ChunkAccum accumulate_chunk(const CompiledProgram& program, std::span<const double> params,
+                            const HyperRect& rect, const StreamKey& key, std::size_t count) {
+  if (!rect.valid()) throw InvalidDomain("invalid hyperrectangle");
+  const mcb::ChunkAccum a = mcb::accumulate_chunk(program_spec(program, params, rect, count < 2 ? 2 : count),
+                                                  key, count, 0);
+  return ChunkAccum{a.n, a.n_nonfinite, a.mean, a.m2};
+}
+
+McEstimate reduce_chunks(double volume, std::span<const ChunkAccum> chunks) {
+  std::vector<mcb::ChunkAccum> c;
+  c.reserve(chunks.size());
+  for (const ChunkAccum& x : chunks) c.push_back(mcb::ChunkAccum{x.n, x.n_nonfinite, x.mean, x.m2});
+  return mcb::reduce_chunks(volume, c);
+}
+
+UniformStream::UniformStream(const StreamKey& key) : key_(key) {
+  if (key.chunk_index > 0xFFFFFFFFull) throw std::out_of_range("chunk_index exceeds 32 bits");
+}
+
+void UniformStream::refill() {
+  // draws = the coordinates of 1-D points on [0, 1): low + 1 * u = u exactly
+  const double lo = 0.0, hi = 1.0;
+  const mcb_status st = mcb_debug_points(key_.global_seed, key_.integrand_index, key_.trial_index, key_.chunk_index,
+                                         drawn_, kBatch, 1, &lo, &hi, 0, buf_.data());
+  if (st != MCB_OK) throw mcb::DeviceError(mcb_last_error());
+  drawn_ += kBatch;
+  pos_ = 0;
+}
+
 McEstimate direct_mc(const CompiledProgram& program, std::span<const double> params, const HyperRect& rect,
                      std::uint64_t n_samples, const StreamKey& key_base) {
   return mcb::direct_mc(program_spec(program, params, rect, n_samples), n_samples, key_base, 0);

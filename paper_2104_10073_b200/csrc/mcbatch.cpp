@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <complex>
 #include <cstdio>
 #include <numbers>
@@ -323,6 +324,62 @@ static std::string trial_error(const mcb_trial_stats& st) {
     case MCB_TRIAL_CHUNK_RANGE: return "chunk_index exceeds 32 bits";
     default: return "every sample evaluated to NaN or infinity";
   }
+}
+
+// ---- per-chunk layer (src/estimator.cpp:9-73) ---------------------------------
+
+void ChunkAccum::add(double x) {
+  if (!std::isfinite(x)) {
+    n_nonfinite += 1;
+    return;
+  }
+  n += 1;
+  const double d = x - mean;  // deviation from the old mean
+  mean = mean + d / double(n);
+  m2 = m2 + d * (x - mean);   // times the deviation from the new one
+}
+
+void ChunkAccum::merge(const ChunkAccum& b) {
+  n_nonfinite += b.n_nonfinite;
+  if (b.n == 0) return;
+  if (n == 0) {
+    n = b.n;
+    mean = b.mean;
+    m2 = b.m2;
+    return;
+  }
+  const std::uint64_t both = n + b.n;
+  const double d = b.mean - mean;
+  mean = mean + d * (double(b.n) / double(both));
+  m2 = m2 + (b.m2 + d * d * (double(n) * double(b.n) / double(both)));
+  n = both;
+}
+
+ChunkAccum accumulate_chunk(const IntegrandSpec& spec, const StreamKey& key, std::size_t count, int device) {
+  if (spec.domain.dim() != spec.dim) throw std::invalid_argument("program/domain dimension mismatch");
+  if (key.chunk_index > 0xFFFFFFFFull) throw std::out_of_range("chunk_index exceeds 32 bits");
+  if (count > kChunkSize) throw std::invalid_argument("count exceeds the chunk size");
+  ProgramCache programs;
+  const mcb_program* prog = spec.family == Family::Program ? programs.get(spec) : nullptr;
+  const mcb_integrand d = to_descriptor(spec, key.integrand_index, prog);
+  mcb_chunk_accum a{};
+  check(mcb_accumulate_chunk(&d, key.global_seed, key.trial_index, key.chunk_index, std::uint32_t(count), device,
+                             &a));
+  return ChunkAccum{a.n, a.n_nonfinite, a.mean, a.m2};
+}
+
+McEstimate reduce_chunks(double volume, std::span<const ChunkAccum> chunks) {
+  ChunkAccum all;
+  for (const ChunkAccum& c : chunks) all.merge(c);
+  if (all.n == 0) throw AllSamplesNonFinite("every sample evaluated to NaN or infinity");
+  McEstimate e;
+  e.n_samples = all.n + all.n_nonfinite;
+  e.n_nonfinite = all.n_nonfinite;
+  e.value = volume * all.mean;
+  e.std_error = all.n >= 2 ? volume * std::sqrt((all.m2 / double(all.n - 1)) / double(all.n))
+                           : std::numeric_limits<double>::infinity();
+  e.nonfinite_warning = double(all.n_nonfinite) > kNonFiniteWarnFraction * double(e.n_samples);
+  return e;
 }
 
 McEstimate direct_mc(const IntegrandSpec& spec, std::uint64_t n_samples, const StreamKey& key_base,

@@ -48,6 +48,7 @@ def load():
         "orc_sample_uniform": (i32, [u32, P(dbl), P(dbl), u64, u32, u32, u64, u64, u64, vp]),
         "orc_eval": (dbl, [P(Integrand), P(dbl)]),
         "orc_accum_add": (None, [P(ChunkAccum), dbl]),
+        "orc_accum_merge": (None, [P(ChunkAccum), P(ChunkAccum)]),
         "orc_accumulate_chunk": (i32, [P(Integrand), u64, u32, u64, u64, P(ChunkAccum)]),
         "orc_volume": (dbl, [P(Integrand)]),
         "orc_chunk_count": (u64, [u64]),
