@@ -346,14 +346,40 @@ CLK_PER_FP64_WARP = 2.0
 N_SM = 148
 
 
-def alu_roofline(samples_per_s: float, sm_mhz, wide=K_DIRECT_WIDE_PER_SAMPLE, fp64=K_DIRECT_FP64_PER_SAMPLE):
+def alu_roofline(samples_per_s: float, sm_mhz, wide=K_DIRECT_WIDE_PER_SAMPLE, fp64=K_DIRECT_FP64_PER_SAMPLE,
+                 clk_per_warp_sample=None):
     """Samples/s against the shared FMA-heavy + FP64 ceiling at the sampled SM clock."""
     if not sm_mhz:
         return None
-    clk_per_warp_sample = wide * CLK_PER_WIDE_WARP + fp64 * CLK_PER_FP64_WARP
+    if clk_per_warp_sample is None:
+        clk_per_warp_sample = wide * CLK_PER_WIDE_WARP + fp64 * CLK_PER_FP64_WARP
     peak = N_SM * 4 * 32 * sm_mhz * 1e6 / clk_per_warp_sample
     return {"achieved": samples_per_s / 1e9, "peak": peak / 1e9, "unit": "G samples/s",
             "frac": samples_per_s / peak, "clk_per_warp_sample": clk_per_warp_sample}
+
+
+# Hot-loop mix of every k_direct instantiation the other configs launch, per
+# loop iteration = one PAIR of samples: (IMAD.WIDE.U32, FP64 ops), keyed by the
+# kernel's template arguments (family, dim, variant) as the launch list names
+# them (profiles/r02_k_direct_costs.txt; checked against the object files by
+# tests/test_bench_roofline.py).  Variants: 0 FAST, 1 FAST unit domain,
+# 11 harmonic unit domain + unit coefficients + folded shift.
+K_DIRECT_PAIR_MIX = {
+    (0, 2, 11): (34, 32), (0, 3, 11): (51, 34), (0, 4, 11): (68, 36), (0, 5, 11): (85, 38),
+    (0, 6, 11): (102, 40), (0, 7, 11): (119, 42),
+    (2, 2, 0): (34, 18), (3, 3, 0): (51, 24), (2, 2, 1): (34, 10), (3, 3, 1): (51, 12),
+}
+
+
+def mix_clk_per_warp_sample(fns, variant_of) -> float:
+    """Sample-weighted FMA-heavy + FP64 clocks per warp-sample of a job whose
+    integrand i runs on k_direct<family, dim, variant_of(f)>."""
+    clk = samples = 0.0
+    for f in fns:
+        wide, fp64 = K_DIRECT_PAIR_MIX[(int(f.family), int(f.dim), variant_of(f))]
+        clk += f.n_samples * (wide * CLK_PER_WIDE_WARP + fp64 * CLK_PER_FP64_WARP) / 2
+        samples += f.n_samples
+    return clk / samples
 
 
 # Philox4x32-10 + the 14-op table harmonic on the shared IMAD.WIDE/FP64 pipe,
@@ -486,8 +512,12 @@ def other_configs(mcb, torch, dev, args, peak_blocks, sm_mhz):
                     "frac_of_philox_peak": info.philox_blocks / secs / peak_blocks,
                     "ok_trials": ok, "trials_total": len(fns) * trials,
                     "timed_launches": reps, "launches_per_run": int(info.launches_per_run)}
-        if key == "C1":  # same kernel as the bench (k_direct<HARMONIC,4,...>)
-            out[key]["alu_roofline"] = alu_roofline(info.total_samples / secs, sm_mhz)
+        # the shared FMA-heavy + FP64 ceiling of the job's own kernel mix (C1: the
+        # bench kernel; C3: FAST abs on boxes; C4/C5: unit-domain harmonic / abs)
+        variant_of = {"C1": lambda f: 11, "C3": lambda f: 0, "C4": lambda f: 11,
+                      "C5": lambda f: 11 if int(f.family) == 0 else 1}[key]
+        out[key]["alu_roofline"] = alu_roofline(info.total_samples / secs, sm_mhz,
+                                                clk_per_warp_sample=mix_clk_per_warp_sample(fns, variant_of))
     return out
 
 

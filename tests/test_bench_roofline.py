@@ -51,6 +51,50 @@ def test_instruction_counts_match_the_compiled_kernel():
     assert re.search(rf"\b{mix['IMAD.WIDE.U32']} IMAD.WIDE.U32", txt)
 
 
+def _max_wide_loop_mix(sass: str) -> Counter:
+    """Mix of the backward-branch loop with the most IMAD.WIDE (the pair loop)."""
+    body = []
+    for line in sass.splitlines():
+        m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
+        if m:
+            body.append((int(m.group(1), 16), m.group(2).strip()))
+    best = Counter()
+    for a, ins in body:
+        t = re.search(r"BRA\s+`?\(?.*?0x([0-9a-f]+)", ins)
+        if "BRA" in ins and t and int(t.group(1), 16) < a:
+            lo = int(t.group(1), 16)
+            c = Counter(re.sub(r"^@!?U?P\w+\s+", "", i).split()[0] for x, i in body if lo <= x <= a)
+            if c["IMAD.WIDE.U32"] > best["IMAD.WIDE.U32"]:
+                best = c
+    return best
+
+
+@pytest.mark.skipif(not (os.path.exists(OBJ) and shutil.which("cuobjdump")), reason="kernel object not built")
+def test_config_kernel_mixes_match_the_compiled_kernels():
+    """bench.K_DIRECT_PAIR_MIX (the per-config ALU ceilings of C3/C4/C5) is the
+    hot-loop mix of each k_direct<family, dim, variant> in the object files."""
+    import bench
+    objs = {0: "direct_harmonic.o", 2: "direct_abs.o", 3: "direct_abs.o"}
+    for (fam, dim, var), (wide, fp64) in bench.K_DIRECT_PAIR_MIX.items():
+        name = f"_ZN3mcb6detail8k_directILi{fam}ELi{dim}ELi{var}EEEvPKNS_3dev6FnDescEPKjmPNS2_11TilePartialE"
+        obj = os.path.join(ROOT, "paper_2104_10073_b200", "csrc", "_obj", objs[fam])
+        sass = subprocess.run(["cuobjdump", "-sass", "-fun", name, obj], capture_output=True, text=True,
+                              check=True).stdout
+        mix = _max_wide_loop_mix(sass)
+        got_fp64 = sum(v for k, v in mix.items() if k.split(".")[0] in ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX"))
+        assert (mix["IMAD.WIDE.U32"], got_fp64) == (wide, fp64), (fam, dim, var)
+
+
+def test_config_mix_ceilings():
+    import bench
+    from paper_2104_10073_b200 import workloads as w
+    fns, _, _ = w.c3()
+    assert bench.mix_clk_per_warp_sample(fns, lambda f: 0) == pytest.approx((49 * 86 + 51 * 126) / 100)
+    fns, _, _ = w.c5(samples=70_000, n_fns=80)
+    clk = bench.mix_clk_per_warp_sample(fns, lambda f: 11 if int(f.family) == 0 else 1)
+    assert clk == pytest.approx((78 + 114 + 100 + 136 + 172 + 208 + 244 + 280) / 8)
+
+
 def test_alu_roofline_arithmetic():
     import bench
     r = bench.alu_roofline(1.8e11, 1965.0)
