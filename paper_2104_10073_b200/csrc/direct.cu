@@ -33,13 +33,23 @@ __global__ void k_expand_tiles(const FnDesc* __restrict__ fns, uint32_t n_fns, u
 
 // Cell volume of stratified cell `cell` (runtime dim; same arithmetic as
 // dev::grid_cell / the reference's grid_cell + HyperRect::volume).
-__device__ double cell_volume(const FnDesc& F, uint32_t cell) {
+// kmag (0: divide): ceil(2^32 / k), exact division of any rem < n_cells by k
+// as (rem * kmag) >> 32 when n_cells * k < 2^32 (the rounding error of kmag is
+// < k, so rem * error stays below 2^32); one multiply instead of a ~15-
+// instruction integer division per axis.
+__device__ __forceinline__ uint64_t cell_div_magic(const FnDesc& F) {
+  const uint64_t k = F.strat_k;
+  return k > 1 && uint64_t(F.n_cells) * k < (1ull << 32) ? ((1ull << 32) + k - 1) / k : 0;
+}
+
+__device__ double cell_volume(const FnDesc& F, uint32_t cell, uint64_t kmag = 0) {
   double w[MCB_MAX_DIM];
   uint32_t rem = cell;
   const uint32_t k = F.strat_k;
   for (int j = int(F.dim) - 1; j >= 0; --j) {
-    const uint32_t digit = rem % k;
-    rem /= k;
+    const uint32_t q = kmag ? uint32_t((uint64_t(rem) * kmag) >> 32) : rem / k;
+    const uint32_t digit = rem - q * k;
+    rem = q;
     if (F.grid_bounds) {  // host-computed boundaries (same arithmetic)
       const double* b = F.grid_bounds + uint32_t(j) * (k + 1) + digit;
       w[j] = __dsub_rn(b[1], b[0]);
@@ -106,10 +116,10 @@ __device__ __forceinline__ void merge_tile(Accum& a, const TilePartial& p) {
 //    lane by lane); the first dead cell (src/batch.cpp:176-180) is the
 //    minimum over lanes.
 __device__ __forceinline__ mcb_trial_stats cell_estimate(const FnDesc& F, const TilePartial* part, uint64_t base,
-                                                         uint32_t c, Accum& a) {
+                                                         uint32_t c, Accum& a, uint64_t kmag) {
   for (uint32_t cc = 0; cc < F.cpc; ++cc) merge_tile(a, part[base + uint64_t(c) * F.cpc + cc]);
   mcb_trial_stats cs;
-  const double vol = F.cell_rects ? rect_volume(F, c) : cell_volume(F, c);
+  const double vol = F.cell_rects ? rect_volume(F, c) : cell_volume(F, c, kmag);
   cs.value = a.n == 0 ? 0.0 : __dmul_rn(vol, a.mean);
   cs.std_error = a.n == 0 ? 0.0
                  : a.n >= 2 ? __dmul_rn(vol, __dsqrt_rn(__ddiv_rn(__ddiv_rn(a.m2, double(a.n - 1)), double(a.n))))
@@ -134,13 +144,19 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
     double value = 0.0, var = 0.0;
     unsigned long long n_all = 0, nn_all = 0;
     uint32_t dead = 0xFFFFFFFFu;
+    const uint64_t kmag = cell_div_magic(F);
+    // a step's 32 cell estimates, read back in cell order by every lane
+    // (shared-memory broadcast); a dead cell enters as (0, 0), which leaves
+    // the sums unchanged — and its trial reports the dead cell, not the sums
+    __shared__ double2 step[4][32];
+    double2* my = step[(threadIdx.x >> 5) & 3];
     for (uint32_t c0 = 0; c0 < F.n_cells; c0 += 32) {
       const uint32_t c = c0 + lane;
       double cv = 0.0, cse2 = 0.0;
       bool live = false;
       if (c < F.n_cells) {
         Accum a;
-        const mcb_trial_stats cs = cell_estimate(F, part, base, c, a);
+        const mcb_trial_stats cs = cell_estimate(F, part, base, c, a, kmag);
         n_all += a.n + a.nn;
         nn_all += a.nn;
         if (F.cell_est) {  // tree round: the cell's own estimate
@@ -160,16 +176,17 @@ __global__ void k_combine(const FnDesc* __restrict__ fns, uint32_t n_fns, uint32
       }
       if (F.cell_est) continue;
       // combine_cells order: the running sums take the cells one by one in
-      // ascending order (broadcast from their lanes), exactly as the reference
-      const uint32_t live_mask = __ballot_sync(0xFFFFFFFFu, live);
-      for (int i = 0; i < 32; ++i) {
-        const double v = __shfl_sync(0xFFFFFFFFu, cv, i);
-        const double w = __shfl_sync(0xFFFFFFFFu, cse2, i);
-        if (live_mask & (1u << i)) {
-          value = __dadd_rn(value, v);
-          var = __dadd_rn(var, w);
-        }
+      // ascending order, exactly as the reference
+      (void)live;
+      my[lane] = make_double2(cv, cse2);
+      __syncwarp();
+      const uint32_t n = min(32u, F.n_cells - c0);
+      for (uint32_t i = 0; i < n; ++i) {
+        const double2 e = my[i];
+        value = __dadd_rn(value, e.x);
+        var = __dadd_rn(var, e.y);
       }
+      __syncwarp();
     }
     if (F.cell_est) {
       if (lane == 0) {
