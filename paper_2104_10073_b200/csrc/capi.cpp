@@ -195,6 +195,10 @@ mcb_status run_sharded(const mcb_integrand* fns, size_t n_fns, uint64_t seed, ui
                        const uint32_t* trial_bases) {
   if (devs.size() > 1 && trials > 1 && !chunk_bases && !trial_bases)
     return run_sharded_trials(fns, n_fns, seed, trials, devs, out);
+  if (devs.size() == 1) {  // one shard: the caller's arrays as they are
+    const mcb_status s = run_shard(fns, n_fns, seed, trials, devs[0], out, chunk_bases, trial_bases);
+    return s == MCB_OK ? s : fail(s, "device " + std::to_string(devs[0]) + ": " + std::string(g_last_error));
+  }
   std::vector<uint32_t> shard(n_fns, 0);
   lpt(fns, n_fns, trials, int(devs.size()), shard.data());
   std::vector<mcb_status> status(devs.size(), MCB_OK);
@@ -395,8 +399,16 @@ void mcb_plan_destroy(mcb_plan* plan) {
 mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
                           const int* devices, int n_devices, mcb_trial_stats* out,
                           double* seconds) {
+  static const bool trace = [] {
+    const char* e = std::getenv("MCB_TREE_TRACE");
+    return e && *e && *e != '0';
+  }();
+  const auto tv0 = std::chrono::steady_clock::now();
   mcb_status st = validate_for_run(fns, n_fns, trials);
   if (st != MCB_OK) return st;
+  if (trace)
+    std::fprintf(stderr, "[mcb run] validate %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tv0).count());
   if (!out) return fail(MCB_ERR_INVALID_ARGUMENT, "out is NULL");
   std::vector<int> devs;
   if (!devices || n_devices <= 0) devs.push_back(0);
@@ -407,7 +419,9 @@ mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<size_t> plain, trees;
   for (size_t i = 0; i < n_fns; ++i) (fns[i].method == MCB_METHOD_TREE ? trees : plain).push_back(i);
-  if (!plain.empty()) {  // direct + stratified: one sharded launch set
+  if (trees.empty()) {  // the common case: no regrouping copies of the job or the results
+    if ((st = run_sharded(fns, n_fns, seed, trials, devs, out, nullptr, nullptr)) != MCB_OK) return st;
+  } else if (!plain.empty()) {  // direct + stratified: one sharded launch set
     std::vector<mcb_integrand> sub(plain.size());
     for (size_t r = 0; r < plain.size(); ++r) sub[r] = fns[plain[r]];
     std::vector<mcb_trial_stats> res(sub.size() * trials);
@@ -425,6 +439,8 @@ mcb_status mcb_run_direct(const mcb_integrand* fns, size_t n_fns, uint64_t seed,
     if ((st = run_trees_on(tasks, seed, devs)) != MCB_OK) return st;
   }
   const auto t1 = std::chrono::steady_clock::now();
+  if (trace)
+    std::fprintf(stderr, "[mcb run] run %.3f ms\n", std::chrono::duration<double, std::milli>(t1 - t0).count());
   if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
   return MCB_OK;
 }

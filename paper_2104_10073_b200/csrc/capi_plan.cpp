@@ -685,6 +685,7 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
   if ((e = grow_pinned(c.h_out, c.h_out_cap, n_out)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
   if ((e = DevBuf::grow(c.buf.bounds, c.buf.cap_bounds, hp.bounds.size())) != cudaSuccess)
     return cuda_fail(e, "cudaMalloc");
+  const auto tq0 = std::chrono::steady_clock::now();
   std::memcpy(c.h_descs, hp.descs.data(), sizeof(FnDesc) * n_fns);
   for (size_t r = 0; r < n_fns; ++r)
     if (hp.bounds_off[r] >= 0) c.h_descs[r].grid_bounds = c.buf.bounds + hp.bounds_off[r];
@@ -696,8 +697,16 @@ mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint
       (e = cudaMemcpyAsync(tile_out, c.buf.part, sizeof(TilePartial) * std::min<size_t>(tile_cap, hp.n_tiles),
                            cudaMemcpyDeviceToHost, c.stream)) != cudaSuccess)
     return cuda_fail(e, "cudaMemcpyAsync(tile partials)");
+  const auto tq1 = std::chrono::steady_clock::now();
   if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  const auto tq2 = std::chrono::steady_clock::now();
   std::memcpy(out, c.h_out, sizeof(mcb_trial_stats) * n_out);
+  const auto tq3 = std::chrono::steady_clock::now();
+  if (trace)
+    std::fprintf(stderr, "[mcb shard] enqueue %.3f ms, sync %.3f ms, copy-out %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(tq1 - tq0).count(),
+                 std::chrono::duration<double, std::milli>(tq2 - tq1).count(),
+                 std::chrono::duration<double, std::milli>(tq3 - tq2).count());
   return MCB_OK;
 }
 
