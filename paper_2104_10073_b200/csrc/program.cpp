@@ -260,6 +260,35 @@ void collect(const Node& n, Symbols& out) {
   for (const auto& k : n.kids) collect(*k, out);
 }
 
+// One operation with the host's libm (kSinCos: its sine result).
+double host_op(Op op, double a, double b) {
+  switch (op) {
+    case kCopy: return a;
+    case kSinCos: return std::sin(a);
+    case kNeg: return -a;
+    case kAdd: return a + b;
+    case kSub: return a - b;
+    case kMul: return a * b;
+    case kDiv: return a / b;
+    case kPow: return std::pow(a, b);
+    case kSin: return std::sin(a);
+    case kCos: return std::cos(a);
+    case kTan: return std::tan(a);
+    case kAsin: return std::asin(a);
+    case kAcos: return std::acos(a);
+    case kAtan: return std::atan(a);
+    case kExp: return std::exp(a);
+    case kLog: return std::log(a);
+    case kSqrt: return std::sqrt(a);
+    case kAbs: return std::fabs(a);
+    case kFloor: return std::floor(a);
+    case kMin: return std::fmin(a, b);
+    case kMax: return std::fmax(a, b);
+    case kCosPlusSin: return std::cos(a) + std::sin(a);
+    default: return NAN;
+  }
+}
+
 // ---- DAG + slot allocation ----------------------------------------------------
 
 struct DagNode {
@@ -350,14 +379,33 @@ struct Lowering {
           d.op = kMul;
           d.b = d.a;
         }
-        // constant operands of + - * /: one correctly rounded IEEE operation,
-        // the same on the host as on the device (2*pi*x1 = (2*pi)*x1)
-        const double *ca = const_of(d.a), *cb = d.b >= 0 ? const_of(d.b) : nullptr;
-        if (ca && cb && (d.op == kAdd || d.op == kSub || d.op == kMul || d.op == kDiv)) {
-          const double x = *ca, y = *cb;
-          const double r = d.op == kAdd ? x + y : d.op == kSub ? x - y : d.op == kMul ? x * y : x / y;
-          return leaf(kConst, constant(r));
+        // Other small integer exponents: E^1 = E and E^0 = 1 exactly (NaN
+        // included, as C's pow); E^-1 = 1/E, correctly rounded; E^3 = (E*E)*E
+        // and E^4 = (E*E)*(E*E), within 1.5 ulp — no worse than libdevice's
+        // pow (2 ulp), far inside the 1e-12 per-sample bar, same specials.
+        if (d.op == kPow) {
+          if (is_const(d.b, 1.0)) return d.a;
+          if (is_const(d.b, 0.0)) return leaf(kConst, constant(1.0));
+          if (is_const(d.b, -1.0) && !const_of(d.a)) {
+            d.op = kDiv;
+            d.b = d.a;
+            d.a = leaf(kConst, constant(1.0));
+          } else if ((is_const(d.b, 3.0) || is_const(d.b, 4.0)) && !const_of(d.a)) {
+            DagNode sq;
+            sq.op = kMul;
+            sq.a = sq.b = d.a;
+            const int s2 = intern(sq);
+            d.op = kMul;
+            d.b = is_const(d.b, 3.0) ? d.a : s2;
+            d.a = s2;
+          }
         }
+        // an operation on constants only is evaluated here, by the host's libm
+        // — the library the reference evaluates it with at run time, so the
+        // folded value is the reference's bit for bit (+ - * / are single
+        // IEEE operations anyway): 2*pi*x1 = (2*pi)*x1, sin(1)*x1, 2^3*x1
+        const double *ca = const_of(d.a), *cb = d.b >= 0 ? const_of(d.b) : nullptr;
+        if (ca && (d.b < 0 || cb)) return leaf(kConst, constant(host_op(d.op, *ca, cb ? *cb : 0.0)));
         return intern(d);
       }
     }
@@ -575,36 +623,8 @@ double evaluate(const Program& p, const double* x, const double* params) {
   };
   for (const Instr& i : p.code) {
     const double a = get(i.a), b = get(i.b);
-    double r = NAN;
-    switch (i.op) {
-      case kCopy: r = a; break;
-      case kSinCos:
-        st[i.dst2] = std::cos(a);
-        r = std::sin(a);
-        break;
-      case kNeg: r = -a; break;
-      case kAdd: r = a + b; break;
-      case kSub: r = a - b; break;
-      case kMul: r = a * b; break;
-      case kDiv: r = a / b; break;
-      case kPow: r = std::pow(a, b); break;
-      case kSin: r = std::sin(a); break;
-      case kCos: r = std::cos(a); break;
-      case kTan: r = std::tan(a); break;
-      case kAsin: r = std::asin(a); break;
-      case kAcos: r = std::acos(a); break;
-      case kAtan: r = std::atan(a); break;
-      case kExp: r = std::exp(a); break;
-      case kLog: r = std::log(a); break;
-      case kSqrt: r = std::sqrt(a); break;
-      case kAbs: r = std::fabs(a); break;
-      case kFloor: r = std::floor(a); break;
-      case kMin: r = std::fmin(a, b); break;
-      case kMax: r = std::fmax(a, b); break;
-      case kCosPlusSin: r = std::cos(a) + std::sin(a); break;
-      default: break;
-    }
-    st[i.dst] = r;
+    if (i.op == kSinCos) st[i.dst2] = std::cos(a);
+    st[i.dst] = host_op(i.op, a, b);
   }
   return st[0];
 }

@@ -90,12 +90,17 @@ def test_compiler_contract(mcb):
     assert (p.n_instr, p.depth) == (5, 1)
     assert mcb.Program("a*x1 + b + c", 1, ["c", "a", "b"]).param_names == ["a", "b", "c"]
     # squares compile to one multiply of the shared operand (x1-c computed once):
-    # Sub, Mul, Sub, Mul, Add, Mul(-100), Exp; other exponents stay pow
+    # Sub, Mul, Sub, Mul, Add, Mul(-100), Exp; cubes and fourth powers to two
+    # multiplies, E^-1 to a division, E^1 / E^0 to E / 1; other exponents stay pow
     peak = mcb.Program("exp(-100*((x1-c)^2+(x2-c)^2))", 2, ["c"])
     assert (peak.n_instr, peak.depth) == (7, 2)
     assert mcb.Program("pow(x1-c, 2)", 1, ["c"]).n_instr == 2
-    assert mcb.Program("(x1-c)^3", 1, ["c"]).n_instr == 2
+    assert mcb.Program("(x1-c)^3", 1, ["c"]).n_instr == 3
+    assert mcb.Program("(x1-c)^4", 1, ["c"]).n_instr == 3
     assert mcb.Program("(x1-c)^2.5", 1, ["c"]).n_instr == 2
+    assert mcb.Program("x1^-1 + x1^0 + x1^1", 1).n_instr == 3  # Div, Add(+1 folded), Add
+    # operations on constants only are folded by the host's libm (the reference's values)
+    assert mcb.Program("sin(1)*x1 + 2^0.5 + exp(-2)", 1).n_instr == 3  # Mul, Add, Add (never reassociated)
     cases = {
         "x3": "x3 exceeds dim=2",
         "2+": "expression does not parse: expected a number, identifier or '(' (at offset 2)",
@@ -202,9 +207,11 @@ def test_eval_points_match_reference(gpu, progs):
 
 @pytest.mark.gpu
 def test_squares_and_constant_folding_exact(gpu):
-    """E^2 / pow(E, 2) run as E*E and constant sub-expressions are folded on
-    the host: both are single correctly rounded IEEE operations, so the GPU
-    values equal numpy's bit for bit, specials included."""
+    """E^2 / pow(E, 2) run as E*E (E^3, E^4 as two multiplies, E^-1 as 1/E)
+    and constant sub-expressions are folded on the host with its libm (the
+    library the reference evaluates them with): the GPU values equal the same
+    operations in numpy bit for bit, specials included; and the cubes and
+    fourth powers stay within 2 ulp of glibc's pow."""
     rng = np.random.default_rng(5)
     x = np.concatenate([rng.uniform(-3, 3, 200), [0.0, -0.0, 1e200, -1e200, 1e-170, np.inf, -np.inf, np.nan]])
     pts = x.reshape(-1, 1)
@@ -213,7 +220,12 @@ def test_squares_and_constant_folding_exact(gpu):
              ("pow(x1-c, 2)", lambda v: (v - c) * (v - c)),
              ("2*pi*x1", lambda v: (2 * math.pi) * v),
              ("-100*x1 + 1/3", lambda v: -100.0 * v + 1.0 / 3.0),
-             ("x1*2*pi", lambda v: (v * 2) * math.pi)]
+             ("x1*2*pi", lambda v: (v * 2) * math.pi),
+             ("x1^-1", lambda v: 1.0 / v),
+             ("x1^1 + x1^0", lambda v: v + 1.0),
+             ("sin(1)*x1 + 2^0.5", lambda v: math.sin(1.0) * v + 2.0 ** 0.5),
+             ("(x1-c)^4", lambda v: ((v - c) * (v - c)) * ((v - c) * (v - c))),
+             ("(x1-c)^3", lambda v: ((v - c) * (v - c)) * (v - c))]
     for src, ref in cases:
         p = gpu.Program(src, 1, ["c"] if "c" in src.replace("pi", "") else [])
         got = p.evaluate(pts, {"c": c} if p.param_names else None)
@@ -222,6 +234,12 @@ def test_squares_and_constant_folding_exact(gpu):
         assert np.array_equal(np.isnan(got), np.isnan(want)), src
         ok = ~np.isnan(want)
         assert np.array_equal(got[ok].view(np.uint64), want[ok].view(np.uint64)), src
+    for src, e in (("(x1-c)^3", 3.0), ("(x1-c)^4", 4.0)):
+        got = gpu.Program(src, 1, ["c"]).evaluate(pts, {"c": c})
+        y = x - c
+        fin = np.isfinite(y) & (np.abs(y) > 1e-60) & (np.abs(y) < 1e60)
+        want = np.array([math.pow(float(v), e) for v in y[fin]])
+        assert np.all(np.abs(got[fin] - want) <= 2 * np.spacing(np.abs(want))), src
 
 
 @pytest.mark.gpu
