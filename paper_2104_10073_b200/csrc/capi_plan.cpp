@@ -506,7 +506,17 @@ uint64_t blocks_per_pair(uint32_t family, uint32_t dim) {
 mcb_status build_host_plan(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
                            uint32_t chunk_base, uint32_t trial_base, HostPlan& hp,
                            const uint32_t* chunk_bases, const uint32_t* trial_bases) {
-  std::vector<Prepared> prep(n_fns);
+  hp.descs.clear();
+  hp.groups.clear();
+  hp.code.clear();
+  hp.consts.clear();
+  hp.bounds.clear();
+  hp.bounds_off.clear();
+  hp.n_tiles = hp.total_samples = hp.philox_blocks = 0;
+  // per-thread scratch: a call reuses the previous call's pages (fresh
+  // vectors of this size are mmap'ed and page-faulted in on every call)
+  thread_local std::vector<Prepared> prep;
+  prep.resize(n_fns);
   for (size_t i = 0; i < n_fns; ++i)
     prep[i] = prepare(fns[i], seed, chunk_bases ? chunk_bases[i] : chunk_base,
                       trial_bases ? trial_bases[i] : trial_base);
@@ -657,7 +667,7 @@ DeviceCtx& device_ctx(int device) {
 mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
                      int device, mcb_trial_stats* out, const uint32_t* chunk_bases,
                      const uint32_t* trial_bases, TilePartial* tile_out, size_t tile_cap) {
-  HostPlan hp;
+  thread_local HostPlan hp;  // reused capacity (see build_host_plan)
   const auto tb0 = std::chrono::steady_clock::now();
   mcb_status st = build_host_plan(fns, n_fns, seed, trials, 0, 0, hp, chunk_bases, trial_bases);
   if (st != MCB_OK) return st;
