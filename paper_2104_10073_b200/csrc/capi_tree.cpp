@@ -268,9 +268,16 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
                   f.family == MCB_FAMILY_PROGRAM ? reinterpret_cast<uintptr_t>(f.program) : uintptr_t(0));
   }
   std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return keys[a] < keys[b]; });
-  HostPlan hp;
-  std::vector<TreeConst> tc(T);
-  std::vector<TreeState> tst(T);
+  // per-thread scratch reused across calls: fresh vectors of this size are
+  // mmap'ed and page-faulted in on every call
+  thread_local HostPlan hp;
+  thread_local std::vector<TreeConst> tc;
+  thread_local std::vector<TreeState> tst;
+  hp.groups.clear();
+  hp.code.clear();
+  hp.consts.clear();
+  tc.resize(T);
+  tst.resize(T);
   std::map<const mcb_program*, std::pair<uint32_t, uint32_t>> prog_at;
   const mcb_program* last_prog = nullptr;
   std::pair<uint32_t, uint32_t> last_at{0, 0};
@@ -419,9 +426,13 @@ mcb_status run_trees_device(std::vector<mcb::tree::TreeTask*>& tasks, uint64_t s
   auto up = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
   };
+  // descriptors through the context's pinned staging (a pageable copy is a
+  // synchronous bounce-buffer transfer)
+  if ((e = grow_pinned(c.h_descs, c.h_descs_cap, T)) != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  std::memcpy(c.h_descs, hp.descs.data(), sizeof(FnDesc) * T);
   if ((e = up(c.t_const, tc.data(), sizeof(TreeConst) * T)) != cudaSuccess ||
       (e = up(c.t_state, tst.data(), sizeof(TreeState) * T)) != cudaSuccess ||
-      (e = up(c.buf.fns, hp.descs.data(), sizeof(FnDesc) * T)) != cudaSuccess ||
+      (e = up(c.buf.fns, c.h_descs, sizeof(FnDesc) * T)) != cudaSuccess ||
       (e = DevBuf::grow(c.buf.rects, c.buf.cap_rects, packed_doubles)) != cudaSuccess ||
       (e = up(c.buf.rects, c.h_rects, sizeof(double) * packed_doubles)) != cudaSuccess ||
       (e = launch_tree_init(c.t_const, c.t_state, L, c.buf.rects, uint32_t(T), s)) != cudaSuccess ||
