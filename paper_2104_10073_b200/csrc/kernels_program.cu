@@ -58,6 +58,10 @@ __device__ __forceinline__ double fetch1(uint32_t kind, uint32_t idx, int h, con
   return kind == prog::kConst ? consts[idx] : params[idx];
 }
 
+// The DSL's exp (dev::mcb_exp, shared with the specialised kernels so both
+// paths stay bit-identical), called rather than inlined into the dispatch.
+__device__ __noinline__ double interp_exp(double a) { return dev::mcb_exp(a); }
+
 // One libm-class operation on one sample.
 __device__ __forceinline__ double call_op(uint32_t op, double a, double b) {
   switch (op) {
@@ -69,7 +73,7 @@ __device__ __forceinline__ double call_op(uint32_t op, double a, double b) {
     case prog::kAsin: return asin(a);
     case prog::kAcos: return acos(a);
     case prog::kAtan: return atan(a);
-    case prog::kExp: return exp(a);
+    case prog::kExp: return interp_exp(a);
     case prog::kLog: return log(a);
     case prog::kCosPlusSin: return dev::cos_plus_sin(a);
     default: return __longlong_as_double(0x7FF8000000000000ll);

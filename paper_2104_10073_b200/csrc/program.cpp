@@ -647,7 +647,7 @@ std::string emit_cuda(const Program& p, const std::string& name) {
     return buf;
   };
   static const char* const unary[] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                      "sin", "cos", "tan", "asin", "acos", "atan", "exp", "log",
+                                      "sin", "cos", "tan", "asin", "acos", "atan", "mcb::dev::mcb_exp", "log",
                                       "__dsqrt_rn", "fabs", "floor"};
   std::string o = "struct " + name + " {\n  static __device__ __forceinline__ double eval(const double* x, "
                   "const double* p) {\n";

@@ -243,6 +243,30 @@ def test_squares_and_constant_folding_exact(gpu):
 
 
 @pytest.mark.gpu
+def test_dsl_exp_accuracy(gpu):
+    """The DSL's exp (dev::mcb_exp: two-term reduction, degree-13 Taylor, the
+    exponent field; libdevice beyond |x| >= 708) within 2 ulp of glibc's exp on
+    [-707.9, 707.9], and glibc's values for the specials, overflow and the
+    subnormal range."""
+    rng = np.random.default_rng(9)
+    x = np.concatenate([rng.uniform(-707.9, 707.9, 20000), rng.uniform(-5, 5, 20000), rng.uniform(-1e-3, 1e-3, 5000),
+                        [0.0, -0.0, 1e-300, 707.99, -707.99, 708.0, -708.0, 709.7, 709.79, 710.0, -744.0,
+                         -746.0, np.inf, -np.inf, np.nan]])
+    got = gpu.Program("exp(x1)", 1).evaluate(x.reshape(-1, 1))
+    def glibc_exp(v):
+        try:
+            return math.exp(v)
+        except OverflowError:
+            return math.inf
+    want = np.array([glibc_exp(v) for v in x])
+    assert np.array_equal(np.isnan(got), np.isnan(x))
+    ok = ~np.isnan(x)
+    fin = ok & np.isfinite(want) & (want > 2.3e-308)
+    assert np.all(np.abs(got[fin] - want[fin]) <= 2 * np.spacing(want[fin]))
+    assert np.all((got[ok & ~fin] == want[ok & ~fin]) | (np.abs(got[ok & ~fin] - want[ok & ~fin]) <= 5e-324))
+
+
+@pytest.mark.gpu
 def test_parameter_scan_failing_value_raises(gpu):
     """A scanned value whose trials all fail makes the scan throw, as in the
     reference (src/batch.cpp:320-329 success rule, :360-364 throw)."""
