@@ -6,7 +6,7 @@
 // whose body is the program's scheduled instruction list as straight-line
 // register code — the same operations, in the same order, as the GPU
 // interpreter executes (kernels_program.cu: __dadd_rn/__dsub_rn/__dmul_rn/
-// __ddiv_rn, libdevice sin/cos/sincos/tan/asin/acos/atan/exp/log/pow, exact
+// __ddiv_rn, libdevice sin/cos/sincos/tan/asin/acos/atan/log/pow, dev::mcb_exp, exact
 // sqrt/fabs/floor/fmin/fmax).  Sample generation, the per-thread pair loop,
 // the non-finite handling and the warp/CTA reduction shapes are exactly
 // those of k_program / k_program_warp with the same CTA size, so every

@@ -13,7 +13,7 @@
 //     words;
 //   * the sample coordinates likewise, X[j][h][tid].
 // Every operation is the reference's: IEEE +,-,*,/ (correctly rounded, as
-// on the host), libdevice sin/cos/tan/asin/acos/atan/exp/log/pow (<= 2 ulp of
+// on the host), libdevice sin/cos/tan/asin/acos/atan/log/pow and dev::mcb_exp (<= 2 ulp of
 // glibc), exact sqrt/fabs/floor/fmin/fmax, and the fused cos + sin of one
 // argument in the Fig. 1 table form (dev::cos_plus_sin).  Points are the same bit-exact
 // Philox stream; non-finite values are counted and skipped.
