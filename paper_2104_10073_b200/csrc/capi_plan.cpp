@@ -662,11 +662,45 @@ DeviceCtx& device_ctx(int device) {
 
 
 // One shard of mcb_run_direct on one device (synchronous).
+// Tiles one trial of an integrand occupies (an upper bound for padded cell
+// grids).
+uint64_t tiles_per_trial(const mcb_integrand& f) {
+  if (!stratified(f)) return chunk_count(f.n_samples);
+  const StratPlan p = stratified_plan(f);
+  return p.n_cells * chunk_count(p.spc) + mcb::detail::kLaneAlign;
+}
+
 // tile_out (may be NULL): also returns the first tile_cap raw tile partials
-// (the chunk accumulators of mcb_accumulate_chunk).
+// (the chunk accumulators of mcb_accumulate_chunk).  A job whose tiles exceed
+// one wave (MCB_WAVE_TILES, default 2^29 tiles = 19 GB of partials and tile
+// table) runs as consecutive waves of whole integrands on the device, each a
+// shard of its own: results are those of one launch set (every (integrand,
+// trial) depends only on its own tiles), memory stays bounded.
 mcb_status run_shard(const mcb_integrand* fns, size_t n_fns, uint64_t seed, uint32_t trials,
                      int device, mcb_trial_stats* out, const uint32_t* chunk_bases,
                      const uint32_t* trial_bases, TilePartial* tile_out, size_t tile_cap) {
+  static const uint64_t wave = [] {
+    const char* e = std::getenv("MCB_WAVE_TILES");
+    const unsigned long long v = e && *e ? std::strtoull(e, nullptr, 10) : 0ull;
+    return v ? uint64_t(v) : (uint64_t(1) << 29);
+  }();
+  if (n_fns > 1 && !tile_out) {
+    uint64_t total = 0;
+    for (size_t i = 0; i < n_fns && total <= wave; ++i) total += tiles_per_trial(fns[i]) * trials;
+    if (total > wave) {
+      for (size_t i0 = 0; i0 < n_fns;) {
+        size_t i1 = i0 + 1;
+        uint64_t acc = tiles_per_trial(fns[i0]) * trials;
+        while (i1 < n_fns && acc + tiles_per_trial(fns[i1]) * trials <= wave) acc += tiles_per_trial(fns[i1++]) * trials;
+        const mcb_status st = run_shard(fns + i0, i1 - i0, seed, trials, device, out + i0 * trials,
+                                        chunk_bases ? chunk_bases + i0 : nullptr,
+                                        trial_bases ? trial_bases + i0 : nullptr);
+        if (st != MCB_OK) return st;
+        i0 = i1;
+      }
+      return MCB_OK;
+    }
+  }
   thread_local HostPlan hp;  // reused capacity (see build_host_plan)
   const auto tb0 = std::chrono::steady_clock::now();
   mcb_status st = build_host_plan(fns, n_fns, seed, trials, 0, 0, hp, chunk_bases, trial_bases);
