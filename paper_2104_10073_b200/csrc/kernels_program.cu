@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ f
 // aligned to kProgThreads by the host), one THREAD per cell (one chunk per
 // cell): sample 0 is the cell's shift, the pairs in ascending order, the
 // cell's TilePartial written by its thread — no reduction.
-template <int D, int V>
+template <int D, int V, int NP>
 __global__ void __launch_bounds__(T) k_program_lane(const FnDesc* __restrict__ fns,
                                                     const uint32_t* __restrict__ tile_fn, uint64_t tile0,
                                                     TilePartial* __restrict__ part,
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(T) k_program_lane(const FnDesc* __restrict__ f
   const uint32_t fi = __ldg(tile_fn + group);
   FnDesc f = fns[fi];
   __shared__ double params[prog::kMaxParams];
-  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  const ProgramSmem m = stage_program<D, NP>(f, code, consts, slots, params);
   const uint64_t tile = group + threadIdx.x;
   const uint32_t rem = uint32_t(tile - f.tile_base);
   const uint32_t trial = rem / f.n_chunks;
@@ -447,22 +447,30 @@ __global__ void __launch_bounds__(T) k_program_lane(const FnDesc* __restrict__ f
   dev::cell_rect<D>(f, cell, 1.0);
   const uint32_t pairs = (count + 1) >> 1;
   const PhiloxPrefix P = dev::make_prefix(f.key0, f.key1, f.chunk_base + cell, f.trial_base + trial);
+  constexpr int NH = 2 * NP;
   double s1 = 0.0, s2 = 0.0;
   uint32_t nbad = 0;
-  for (uint32_t q = 0; q < pairs; ++q) {
-    gen_points<D, false>(f, P, q, m.X);
-    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
-    const double f0 = m.S[threadIdx.x], f1 = m.S[T + threadIdx.x];
-    if (q == 0) f.shift = finite64(f0) ? f0 : 0.0;
-    const bool has1 = 2 * q + 1 < count;
-    const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
-    nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
-    const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
-    const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
-    s1 = __dadd_rn(s1, g0);
-    s2 = fma(g0, g0, s2);
-    s1 = __dadd_rn(s1, g1);
-    s2 = fma(g1, g1, s2);
+  // NP consecutive pairs of the cell per dispatch, taken in ascending order
+  // (so the sums, and the results, do not depend on NP)
+  for (uint32_t q0 = 0; q0 < pairs; q0 += NP) {
+    gen_points<D, false, NP>(f, P, q0, m.X, 1);
+    interp<NH>(m.code, f.prog_len, m.consts, params, m.S, m.X);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const uint32_t q = q0 + uint32_t(i);
+      if (q >= pairs) break;
+      const double f0 = m.S[2 * i * T + threadIdx.x], f1 = m.S[(2 * i + 1) * T + threadIdx.x];
+      if (q == 0) f.shift = finite64(f0) ? f0 : 0.0;
+      const bool has1 = 2 * q + 1 < count;
+      const bool ok0 = finite64(f0), ok1 = has1 && finite64(f1);
+      nbad += (ok0 ? 0u : 1u) + ((has1 && !ok1) ? 1u : 0u);
+      const double g0 = ok0 ? __dsub_rn(f0, f.shift) : 0.0;
+      const double g1 = ok1 ? __dsub_rn(f1, f.shift) : 0.0;
+      s1 = __dadd_rn(s1, g0);
+      s2 = fma(g0, g0, s2);
+      s1 = __dadd_rn(s1, g1);
+      s2 = fma(g1, g1, s2);
+    }
   }
   TilePartial p;
   p.s1 = s1;
@@ -526,14 +534,14 @@ using ProgFn = void (*)(const FnDesc*, const uint32_t*, uint64_t, TilePartial*, 
 using ProgEvalFn = void (*)(const FnDesc*, const uint32_t*, const double*, uint32_t, uint32_t,
                             uint32_t, uint32_t, uint32_t, double*);
 
-// Pairs per dispatch of the CTA-per-tile kernels (modes 0-2): index of
-// NP = 1, 2, 4.
+// Pairs per dispatch of the CTA-per-tile and lane-per-cell kernels (modes
+// 0-2, 4): index of NP = 1, 2, 4.
 constexpr int kNpVariants = 3;
 constexpr int np_of(int i) { return 1 << i; }
 
 struct ProgEntry {
   ProgFn run = nullptr;               // NP = 1 (every mode)
-  ProgFn run_np[kNpVariants] = {};    // modes 0-2 by NP index
+  ProgFn run_np[kNpVariants] = {};    // modes 0-2 and 4 by NP index
   ProgEvalFn eval = nullptr;
 };
 
@@ -555,7 +563,13 @@ struct ProgTable {
     e[D][1] = tile_entry<D, kSafe | kUnitDomain>(k_program_eval<D, kSafe | kUnitDomain>);
     e[D][2] = tile_entry<D, kSafe | kStrat>(k_program_eval<D, kSafe>);
     e[D][3] = {k_program_warp<D, kSafe | kStrat | kWarpTile>, {}, k_program_eval<D, kSafe>};
-    e[D][4] = {k_program_lane<D, kSafe | kStrat | kLaneCell>, {}, k_program_eval<D, kSafe>};
+    ProgEntry lane;
+    lane.run = k_program_lane<D, kSafe | kStrat | kLaneCell, 1>;
+    lane.run_np[0] = k_program_lane<D, kSafe | kStrat | kLaneCell, 1>;
+    lane.run_np[1] = k_program_lane<D, kSafe | kStrat | kLaneCell, 2>;
+    lane.run_np[2] = k_program_lane<D, kSafe | kStrat | kLaneCell, 4>;
+    lane.eval = k_program_eval<D, kSafe>;
+    e[D][4] = lane;
   }
   ProgTable() {
     put<1>();
@@ -609,7 +623,7 @@ static cudaError_t ensure_smem_optin() {
 // resident per SM; MCB_INTERP_NP=1|2|4 forces it (ablation).
 constexpr size_t kInterpSmemBudget = 56 * 1024;
 static int interp_np_index(uint32_t slots, int dim, int mode) {
-  if (mode > 2) return 0;
+  if (mode == 3) return 0;  // warp-per-tile cells: one pair per lane per dispatch
   static const int forced = [] {
     const char* v = std::getenv("MCB_INTERP_NP");
     return v ? std::atoi(v) : 0;

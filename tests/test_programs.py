@@ -543,6 +543,9 @@ for i, (s, d, p) in enumerate(srcs):
     fns.append(prog.integrand(p, low=[-0.5] * d, high=[1.5] * d, n_samples=70_000, index=10 + i))
 fns.append(mcb.stratify(keep[1].integrand({}, low=[-1, 0, 0], high=[1, 2, 1], n_samples=300_000, index=30),
                         cells_per_dim=2))
+# >= 1024 small cells: the lane-per-cell interpreter kernel (mode 4), odd samples per cell
+fns.append(mcb.stratify(keep[0].integrand({"k": 31.5}, n_samples=1_000_000, index=31)))
+fns.append(mcb.stratify(keep[1].integrand({}, n_samples=500_000, index=32), cells_per_dim=11))
 out = mcb.run_direct(fns, 4242, 3)
 print(hashlib.sha256(out.tobytes()).hexdigest())
 """
