@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(T) k_program(const FnDesc* __restrict__ fns,
 // one (integrand, trial) — the host pads per-trial tile ranges to multiples
 // of kTileAlign — so the staged program stays CTA-uniform while each warp
 // runs one tile: per-warp shift, lane-strided pairs, warp butterfly.
-template <int D, int V>
+template <int D, int V, int NP>
 __global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ fns,
                                                     const uint32_t* __restrict__ tile_fn, uint64_t tile0,
                                                     TilePartial* __restrict__ part,
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ f
   const uint32_t fi = __ldg(tile_fn + group);
   FnDesc f = fns[fi];
   __shared__ double params[prog::kMaxParams];
-  const ProgramSmem m = stage_program<D>(f, code, consts, slots, params);
+  const ProgramSmem m = stage_program<D, NP>(f, code, consts, slots, params);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t tile = group + warp;
   const uint32_t rem = uint32_t(tile - f.tile_base);
@@ -387,22 +387,21 @@ __global__ void __launch_bounds__(T) k_program_warp(const FnDesc* __restrict__ f
     s1 = __dadd_rn(s1, g1);
     s2 = fma(g1, g1, s2);
   };
-  {  // first pair of every lane; lane 0's sample 0 is the per-tile shift
-    double f0 = 0.0, f1 = 0.0;
-    if (lane < pairs) {
-      gen_points<D, false>(f, P, lane, m.X);
-      interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
-      f0 = m.S[threadIdx.x];
-      f1 = m.S[T + threadIdx.x];
+  // each lane's pairs q = lane + 32 k in ascending k, NP of them per dispatch
+  // (results do not depend on NP); lane 0's sample 0 is the per-tile shift
+  constexpr int NH = 2 * NP;
+  for (uint32_t q0 = lane; q0 < pairs || q0 == uint32_t(lane); q0 += 32 * NP) {
+    gen_points<D, false, NP>(f, P, q0, m.X, 32);
+    interp<NH>(m.code, f.prog_len, m.consts, params, m.S, m.X);
+    if (q0 == uint32_t(lane)) {  // first dispatch of every lane (warp-uniform)
+      const double c = __shfl_sync(0xFFFFFFFFu, m.S[threadIdx.x], 0);
+      f.shift = finite64(c) ? c : 0.0;
     }
-    const double c = __shfl_sync(0xFFFFFFFFu, f0, 0);
-    f.shift = finite64(c) ? c : 0.0;
-    if (lane < pairs) add(lane, f0, f1);
-  }
-  for (uint32_t q = lane + 32; q < pairs; q += 32) {
-    gen_points<D, false>(f, P, q, m.X);
-    interp_pair(m.code, f.prog_len, m.consts, params, m.S, m.X);
-    add(q, m.S[threadIdx.x], m.S[T + threadIdx.x]);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const uint32_t q = q0 + 32u * uint32_t(i);
+      if (q < pairs) add(q, m.S[2 * i * T + threadIdx.x], m.S[(2 * i + 1) * T + threadIdx.x]);
+    }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -534,14 +533,14 @@ using ProgFn = void (*)(const FnDesc*, const uint32_t*, uint64_t, TilePartial*, 
 using ProgEvalFn = void (*)(const FnDesc*, const uint32_t*, const double*, uint32_t, uint32_t,
                             uint32_t, uint32_t, uint32_t, double*);
 
-// Pairs per dispatch of the CTA-per-tile and lane-per-cell kernels (modes
-// 0-2, 4): index of NP = 1, 2, 4.
+// Pairs per dispatch of the interpreter kernels (every mode): index of
+// NP = 1, 2, 4.
 constexpr int kNpVariants = 3;
 constexpr int np_of(int i) { return 1 << i; }
 
 struct ProgEntry {
   ProgFn run = nullptr;               // NP = 1 (every mode)
-  ProgFn run_np[kNpVariants] = {};    // modes 0-2 and 4 by NP index
+  ProgFn run_np[kNpVariants] = {};    // by NP index
   ProgEvalFn eval = nullptr;
 };
 
@@ -562,7 +561,13 @@ struct ProgTable {
     e[D][0] = tile_entry<D, kSafe>(k_program_eval<D, kSafe>);
     e[D][1] = tile_entry<D, kSafe | kUnitDomain>(k_program_eval<D, kSafe | kUnitDomain>);
     e[D][2] = tile_entry<D, kSafe | kStrat>(k_program_eval<D, kSafe>);
-    e[D][3] = {k_program_warp<D, kSafe | kStrat | kWarpTile>, {}, k_program_eval<D, kSafe>};
+    ProgEntry warp;
+    warp.run = k_program_warp<D, kSafe | kStrat | kWarpTile, 1>;
+    warp.run_np[0] = k_program_warp<D, kSafe | kStrat | kWarpTile, 1>;
+    warp.run_np[1] = k_program_warp<D, kSafe | kStrat | kWarpTile, 2>;
+    warp.run_np[2] = k_program_warp<D, kSafe | kStrat | kWarpTile, 4>;
+    warp.eval = k_program_eval<D, kSafe>;
+    e[D][3] = warp;
     ProgEntry lane;
     lane.run = k_program_lane<D, kSafe | kStrat | kLaneCell, 1>;
     lane.run_np[0] = k_program_lane<D, kSafe | kStrat | kLaneCell, 1>;
@@ -623,7 +628,6 @@ static cudaError_t ensure_smem_optin() {
 // resident per SM; MCB_INTERP_NP=1|2|4 forces it (ablation).
 constexpr size_t kInterpSmemBudget = 56 * 1024;
 static int interp_np_index(uint32_t slots, int dim, int mode) {
-  if (mode == 3) return 0;  // warp-per-tile cells: one pair per lane per dispatch
   static const int forced = [] {
     const char* v = std::getenv("MCB_INTERP_NP");
     return v ? std::atoi(v) : 0;

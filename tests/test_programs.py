@@ -546,6 +546,9 @@ fns.append(mcb.stratify(keep[1].integrand({}, low=[-1, 0, 0], high=[1, 2, 1], n_
 # >= 1024 small cells: the lane-per-cell interpreter kernel (mode 4), odd samples per cell
 fns.append(mcb.stratify(keep[0].integrand({"k": 31.5}, n_samples=1_000_000, index=31)))
 fns.append(mcb.stratify(keep[1].integrand({}, n_samples=500_000, index=32), cells_per_dim=11))
+# small cells of a small grid (warp per tile, mode 3) and a tree (its rounds run mode 3 too)
+fns.append(mcb.stratify(keep[1].integrand({}, n_samples=200_001, index=33), cells_per_dim=5))
+fns.append(mcb.tree(keep[2].integrand({"a": 1.5}, n_samples=60_000, index=34), samples_per_cell=300))
 out = mcb.run_direct(fns, 4242, 3)
 print(hashlib.sha256(out.tobytes()).hexdigest())
 """
