@@ -111,6 +111,27 @@ def test_compute_without_device_fails_loudly(mcb):
         mcb.debug_points(1, 0, 0, 0, 0, 4, [0.0], [1.0])
 
 
+def test_accumulate_chunk_argument_errors(mcb):
+    """mcb_accumulate_chunk rejects bad arguments before touching a device
+    (count above the chunk size, a chunk index past 32 bits, an invalid
+    descriptor); a zero count is an empty accumulator on any machine."""
+    f = mcb.harmonic(2.0, 2, n_samples=10)
+    for args in ((1, 0, 0, 65537), (1, 0, 2**32, 10)):
+        with pytest.raises(mcb.McbError) as e:
+            mcb.accumulate_chunk(f, *args)
+        assert e.value.status in (1, 5), str(e.value)  # invalid argument / out of range
+    bad = mcb.harmonic(2.0, 2, low=[0.0, 1.0], high=[1.0, 0.5], n_samples=10)
+    with pytest.raises(mcb.McbError) as e:
+        mcb.accumulate_chunk(bad, 1, 0, 0, 100)
+    assert e.value.status == 2 and "domain is invalid" in str(e.value)
+    z = mcb.accumulate_chunk(f, 1, 0, 0, 0)
+    assert (z.n, z.n_nonfinite, z.mean, z.m2) == (0, 0, 0.0, 0.0)
+    if mcb.device_count() == 0:
+        with pytest.raises(mcb.McbError) as e:
+            mcb.accumulate_chunk(f, 1, 0, 0, 100)
+        assert e.value.status == 4  # MCB_ERR_NO_DEVICE: no CPU fallback
+
+
 def test_validation_error_precedes_device_check(mcb):
     with pytest.raises(mcb.McbError) as e:
         mcb.run_direct([mcb.harmonic(2.0, 2, n_samples=1)], 1, 2)
